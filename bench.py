@@ -1,0 +1,430 @@
+#!/usr/bin/env python3
+"""Headline benchmark: frames/s and Gsamples/s of the per-pixel raycaster.
+
+Workload (BASELINE.json configs[2], "C3"): 512^3 uint16 synthetic CT phantom
+(3-D Shepp-Logan), 1920x1080, Zucker-Hummel gradients, composited with early
+ray termination, camera orbiting 1 degree per frame (the reference bench
+convention, bench.py:110-117).  A "step" is one frame.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched by torchrun, one rank per GPU: every frame is split into
+interleaved row bands across the ranks (the volume is replicated) and the
+bands are gathered over NVLink with NCCL (paper_1609_01317_b200.dispatch).
+
+Our arm prints one JSON line with value (device fps, inputs resident),
+e2e (fps through the public render_frame API with the frame copied to
+pinned host memory), roofline, cpu_baseline, clocks, gpu_launches.
+--impl reference times the reference's CPU algorithm (the C oracle port,
+all host threads) on a bounded sample of the same frames.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "frames/sec and Gsamples/s, 512³ volume @1920×1080, at 1/2/4/8 B200 vs CPU ref"
+UNIT = "frames/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--size", type=int, default=512)
+    ap.add_argument("--width", type=int, default=1920)
+    ap.add_argument("--height", type=int, default=1080)
+    ap.add_argument("--op", default="zucker-hummel")
+    ap.add_argument("--mode", default="composited")
+    ap.add_argument("--grad", default="volume", choices=("taps", "volume"))
+    ap.add_argument("--no-skip", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU time of the bounded cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def lscpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def profiled_traffic():
+    p = ROOT / "profiles" / "raycast_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            return None
+    return None
+
+
+def build_workload(args):
+    import paper_1609_01317_b200 as vc
+    from paper_1609_01317_b200 import phantoms
+
+    vol = phantoms.ct_phantom(args.size)
+    op = vc.OperatorKind(args.op)
+
+    def frame(i):
+        sc, st = phantoms.scene_c3(vol, op=op, width=args.width, height=args.height,
+                                   azimuth=float(i), mode=args.mode)
+        from dataclasses import replace
+
+        return sc, replace(st, gradient_source=args.grad, use_octree=not args.no_skip)
+
+    return vol, frame
+
+
+# ------------------------------------------------------------------ CPU legs
+
+def cpu_sample_fps(vol, frame, first_frame: int, target_s: float, threads: int):
+    """Time the C oracle port (the reference algorithm, brute force) on a
+    bounded, evenly spread subset of rows of consecutive orbit frames."""
+    from oracle import oracle
+    from tests.specs import spec_of
+
+    arr = vol.as_array()
+    sc, st = frame(first_frame)
+    H = st.height
+    nb = 8  # rows per band
+    # estimate with a small sample, then size the real sample to target_s
+    done_rows = 0
+    spent = 0.0
+    bands_used = 0
+    stride = 16
+    order = list(range(0, H // nb, stride))
+    f = first_frame
+    t_start = time.perf_counter()
+    while True:
+        for b in order:
+            sc, st = frame(f)
+            spec = spec_of((sc, st))
+            t0 = time.perf_counter()
+            oracle.render(arr, vol.spacing, spec, threads=threads, rows=(b * nb, b * nb + nb))
+            spent += time.perf_counter() - t0
+            done_rows += nb
+            bands_used += 1
+            f += 1
+            if spent >= target_s:
+                break
+        if spent >= target_s or time.perf_counter() - t_start > 3 * target_s:
+            break
+    frame_seconds = spent / done_rows * H
+    return 1.0 / frame_seconds, f"{done_rows} rows in {bands_used} bands of {nb} rows, evenly spread " \
+                                f"over frames {first_frame}..{f - 1} ({spent:.1f} s CPU wall)"
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    vol, frame = build_workload(args)
+    threads = os.cpu_count() or 1
+    from oracle import oracle
+
+    oracle.build()
+    per_step = max(args.cpu_seconds / 4.0, 1.0)
+    fps_list = []
+    for i in range(args.warmup + args.steps):
+        fps, sample = cpu_sample_fps(vol, frame, i * 7, per_step, threads)
+        if i >= args.warmup:
+            fps_list.append(fps)
+    value = statistics.median(fps_list)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"C3: {args.size}^3 uint16 CT phantom, {args.width}x{args.height}, "
+                               f"{args.op}, {args.mode}, brute force (reference C port)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"per step: {sample}; cpu: {lscpu_model()}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def run_ours(args):
+    import ctypes
+
+    import torch
+
+    import paper_1609_01317_b200 as vc
+    from paper_1609_01317_b200 import _native
+    from paper_1609_01317_b200.raycast import render_params, sample_count_of
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = local
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    vol, frame = build_workload(args)
+    L = _native.load(build_if_missing=False)
+    dv = vc.device_volume(vol, dev)
+    sc0, st0 = frame(0)
+    H, W = st0.height, st0.width
+    if st0.gradient_source == "volume":
+        dv.gradient_prepass(st0.operator.code)
+    stream = torch.cuda.current_stream(dev)
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{dev}")
+
+    from paper_1609_01317_b200.dispatch import BandPlan, TileGather
+
+    plan = BandPlan(H, W, band_rows=8, world=world, rank=rank)
+    local_buf = torch.empty((max(plan.local_rows, 1), W, 4), dtype=torch.uint8, device=f"cuda:{dev}")
+    gather = TileGather(plan, device=f"cuda:{dev}") if world > 1 else None
+
+    def render(i, counters=None):
+        sc, st = frame(i)
+        P = render_params(vol, sc, st, band_rows=plan.band_rows, band_first=rank, band_step=world)
+        _native.check(L.vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(local_buf.data_ptr()),
+                                  counters, sp))
+        if gather is not None:
+            return gather(local_buf)
+        return local_buf
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    for i in range(args.warmup):
+        render(i)
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(dev) as clk:
+        barrier()
+        t_wall = time.perf_counter()
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush between timed frames (outside the event pair)
+            ev[k][0].record(stream)
+            render(args.warmup + k)
+            ev[k][1].record(stream)
+        barrier()
+        t_wall = time.perf_counter() - t_wall
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms_local = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([ms_local], dtype=torch.float64, device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_total = float(t.item())
+    else:
+        ms_total = ms_local
+    fps = args.steps / (ms_total / 1000.0)
+
+    # brute-force work counts of the timed frames (our skip-off counts equal
+    # the reference's sample counts, tests/test_gpu_parity.py), untimed
+    cnt = torch.zeros(4, dtype=torch.int64, device=f"cuda:{dev}")
+    Wt = Kt = 0
+    nsub = min(args.steps, 6)
+    for k in range(nsub):
+        sc, st = frame(args.warmup + k)
+        from dataclasses import replace
+
+        P = render_params(vol, sc, replace(st, use_octree=False, gradient_source="taps"),
+                          band_rows=plan.band_rows, band_first=rank, band_step=world)
+        _native.check(L.vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(local_buf.data_ptr()),
+                                  ctypes.c_void_p(cnt.data_ptr()), sp))
+        torch.cuda.synchronize(dev)
+        c = cnt.cpu().numpy()
+        Wt += int(c[0]) + int(c[1])
+        Kt += int(c[1])
+    if world > 1:
+        t = torch.tensor([Wt, Kt], dtype=torch.int64, device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t)
+        Wt, Kt = (int(x) for x in t.cpu().numpy())
+    w_frame = Wt / nsub
+    k_frame = Kt / nsub
+
+    # executed work of the timed configuration (skipping on)
+    sc, st = frame(args.warmup)
+    P = render_params(vol, sc, st, band_rows=plan.band_rows, band_first=rank, band_step=world)
+    _native.check(L.vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(local_buf.data_ptr()),
+                              ctypes.c_void_p(cnt.data_ptr()), sp))
+    torch.cuda.synchronize(dev)
+    ce = cnt.cpu().numpy().tolist()
+
+    # parity spot check of the timed configuration vs the bit-faithful taps path
+    parity = None
+    if rank == 0:
+        img_fast = vc.render_frame(vol, *frame(args.warmup), device=dev).pixels
+        sc, st = frame(args.warmup)
+        from dataclasses import replace
+
+        img_ref = vc.render_frame(vol, sc, replace(st, gradient_source="taps", use_octree=False),
+                                  device=dev).pixels
+        parity = {"max_abs_diff_vs_fp64_taps_bruteforce": int(np.abs(
+            img_fast.astype(int) - img_ref.astype(int)).max()),
+            "pixels_differing": int((img_fast != img_ref).any(axis=2).sum())}
+
+    # end to end through the public API: render_frame into pinned host memory
+    e2e = None
+    if not args.no_e2e and world == 1:
+        pinned = torch.empty((H, W, 4), dtype=torch.uint8, pin_memory=True)
+        out = pinned.numpy()
+        for i in range(2):
+            vc.render_frame(vol, *frame(i), device=dev, out=out)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            vc.render_frame(vol, *frame(args.warmup + k), device=dev, out=out)
+        t_e2e = time.perf_counter() - t0
+        e2e = {"value": args.steps / t_e2e, "unit": UNIT,
+               "h2d_bytes_per_step": ctypes.sizeof(_native.RenderParams),
+               "d2h_bytes_per_step": H * W * 4 + 8 * _native.NUM_COUNTERS,
+               "path": "paper_1609_01317_b200.render_frame(volume resident, out=pinned host)"}
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        threads = os.cpu_count() or 1
+        cfps, sample = cpu_sample_fps(vol, frame, args.warmup, args.cpu_seconds, threads)
+        cpu = {"value": cfps, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"C oracle port of _kernels.render_tile (brute force, float64), {sample}; "
+                         f"cpu: {lscpu_model()}"}
+
+    bpv = vol.data.dtype.itemsize
+    alg_bytes = 8 * bpv * w_frame + 128 * k_frame + 4 * H * W
+    avg_ms = float(np.mean(step_ms))
+    achieved = alg_bytes / (avg_ms / 1000.0) / 1e9
+    peak, peak_kind = peaks()
+    traffic = profiled_traffic()
+    line = {
+        "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C3: {args.size}^3 uint16 3-D Shepp-Logan CT phantom, "
+                               f"{W}x{H}, {args.op}, {args.mode}, 1 deg/frame orbit",
+                   "volume": f"{args.size}^3 uint16", "image": f"{W}x{H}", "operator": args.op,
+                   "mode": args.mode, "gradient_source": args.grad,
+                   "empty_space_skipping": not args.no_skip,
+                   "l2": "flushed between timed frames (256 MiB write, outside the event pair)",
+                   "parallelism": f"image-plane row bands x{world}"},
+        "gsamples_per_s": w_frame * fps / 1e9,
+        "work_per_frame": {"W_ray_samples_bruteforce": w_frame, "K_shades": k_frame,
+                           "executed": {"samples": ce[0], "shades": ce[1], "skipped": ce[2],
+                                        "rays_in_box": ce[3]}},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": (traffic or {}).get("bytes_per_launch"),
+                     "kernel": "vc::raycast_kernel", "peak_source": peak_kind,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "note": "logical bytes 8*bpv*W + 128*K + 4*pixels (SURVEY.md 8(d)); the kernel "
+                             "is gather/FP64 bound, HBM is the stated denominator"},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+        "parity": parity,
+        "wall_s_timed_region": t_wall,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

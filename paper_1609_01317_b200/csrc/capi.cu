@@ -1,0 +1,464 @@
+// capi.cu -- the C ABI (include/voxelcast_b200.h): device-resident volume
+// objects, their caches, and the launch wrappers.
+//
+// A vc_volume owns, on one device:
+//   * the voxel grid (immutable after create; the reference Volume is frozen,
+//     volume.py:47, :71-72)
+//   * the 8^3 macrocell min/max grid (built once) and the occupancy bytes of
+//     the last threshold window (rebuilt only when the window changes)
+//   * one packed float4 gradient volume per operator (Kernel 1, lazily)
+//   * scratch for the host-facing render path.
+// The reference API is stateless per call (raycast.py:431-438); keeping the
+// upload and the derived grids on the volume object is what lets a frame be
+// a single kernel launch.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "vc_internal.h"
+
+struct vc_volume {
+    int device = 0;
+    int dtype = VC_U16;
+    int nx = 0, ny = 0, nz = 0;
+    double spacing[3] = {1.0, 1.0, 1.0};
+    void* d_data = nullptr;
+    size_t bytes = 0;
+    float2* d_mm = nullptr;
+    uint8_t* d_occ = nullptr;
+    int mx = 0, my = 0, mz = 0;
+    bool occ_valid = false;
+    double occ_lo = 0.0, occ_hi = 0.0;
+    float4* d_grad[3] = {nullptr, nullptr, nullptr};
+    uint8_t* d_scratch = nullptr;
+    size_t scratch_bytes = 0;
+    uint64_t* d_counters = nullptr;
+    cudaStream_t host_stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::mutex mu;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(VC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define VC_CUDA(call)                                   \
+    do {                                                \
+        cudaError_t _e = (call);                        \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+    } while (0)
+
+size_t dtype_size(int dtype) { return dtype == VC_U8 ? 1 : (dtype == VC_U16 ? 2 : 4); }
+
+bool is_pow2(double s) {
+    int e = 0;
+    return std::frexp(s, &e) == 0.5;
+}
+
+vc::RayPos make_raypos(const vc_volume* v) {
+    vc::RayPos rp{};
+    bool pow2 = true;
+    for (int a = 0; a < 3; a++) {
+        rp.s[a] = v->spacing[a];
+        rp.rs[a] = 1.0 / v->spacing[a];
+        pow2 = pow2 && is_pow2(v->spacing[a]);
+    }
+    rp.pow2 = pow2;
+    return rp;
+}
+
+class DeviceGuard {
+   public:
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev_);
+        if (prev_ != dev) cudaSetDevice(dev);
+        dev_ = dev;
+    }
+    ~DeviceGuard() {
+        if (prev_ != dev_) cudaSetDevice(prev_);
+    }
+
+   private:
+    int prev_ = 0, dev_ = 0;
+};
+
+int validate_dims(int dtype, int nx, int ny, int nz, const double* spacing) {
+    if (dtype < VC_U8 || dtype > VC_F32) return fail(VC_ERR_INVALID, "dtype must be VC_U8, VC_U16 or VC_F32");
+    if (nx <= 0 || ny <= 0 || nz <= 0) return fail(VC_ERR_INVALID, "volume must contain at least one voxel");
+    if ((double)nx * ny * nz > 4294967295.0)
+        return fail(VC_ERR_UNSUPPORTED, "volumes above 2^32 - 1 voxels are not supported");
+    if (spacing == nullptr) return fail(VC_ERR_INVALID, "spacing is required");
+    for (int a = 0; a < 3; a++)
+        if (!(spacing[a] > 0.0) || !std::isfinite(spacing[a]))
+            return fail(VC_ERR_INVALID, "spacing must be positive");
+    return VC_OK;
+}
+
+int finish_create(vc_volume* v) {
+    // macrocells over interpolation cells [0, max(n-2,0)] per axis
+    v->mx = std::max(v->nx - 2, 0) / 8 + 1;
+    v->my = std::max(v->ny - 2, 0) / 8 + 1;
+    v->mz = std::max(v->nz - 2, 0) / 8 + 1;
+    const size_t mc = (size_t)v->mx * v->my * v->mz;
+    VC_CUDA(cudaMalloc(&v->d_mm, mc * sizeof(float2)));
+    VC_CUDA(cudaMalloc(&v->d_occ, mc));
+    VC_CUDA(cudaMalloc(&v->d_counters, VC_NUM_COUNTERS * sizeof(uint64_t)));
+    VC_CUDA(cudaStreamCreateWithFlags(&v->host_stream, cudaStreamNonBlocking));
+    VC_CUDA(cudaEventCreate(&v->ev0));
+    VC_CUDA(cudaEventCreate(&v->ev1));
+    VC_CUDA(vc::launch_macrocell_minmax(v->dtype, v->d_data, v->nx, v->ny, v->nz, v->d_mm, v->mx, v->my,
+                                        v->mz, v->host_stream));
+    VC_CUDA(cudaStreamSynchronize(v->host_stream));
+    return VC_OK;
+}
+
+void release(vc_volume* v) {
+    if (!v) return;
+    DeviceGuard g(v->device);
+    cudaFree(v->d_data);
+    cudaFree(v->d_mm);
+    cudaFree(v->d_occ);
+    for (auto& p : v->d_grad) cudaFree(p);
+    cudaFree(v->d_scratch);
+    cudaFree(v->d_counters);
+    if (v->host_stream) cudaStreamDestroy(v->host_stream);
+    if (v->ev0) cudaEventDestroy(v->ev0);
+    if (v->ev1) cudaEventDestroy(v->ev1);
+    delete v;
+}
+
+int create_common(int device, const void* src, cudaMemcpyKind kind, int dtype, int nx, int ny, int nz,
+                  const double spacing[3], vc_volume** out) {
+    if (out == nullptr) return fail(VC_ERR_INVALID, "out is null");
+    *out = nullptr;
+    if (src == nullptr) return fail(VC_ERR_INVALID, "volume data is null");
+    int rc = validate_dims(dtype, nx, ny, nz, spacing);
+    if (rc) return rc;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(VC_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+    if (device < 0 || device >= ndev) return fail(VC_ERR_INVALID, "device ordinal out of range");
+    DeviceGuard g(device);
+    vc_volume* v = new vc_volume();
+    v->device = device;
+    v->dtype = dtype;
+    v->nx = nx;
+    v->ny = ny;
+    v->nz = nz;
+    for (int a = 0; a < 3; a++) v->spacing[a] = spacing[a];
+    v->bytes = (size_t)nx * ny * nz * dtype_size(dtype);
+    cudaError_t e = cudaMalloc(&v->d_data, v->bytes);
+    if (e != cudaSuccess) {
+        release(v);
+        return fail(VC_ERR_NOMEM, std::string("cudaMalloc(volume): ") + cudaGetErrorString(e));
+    }
+    e = cudaMemcpy(v->d_data, src, v->bytes, kind);
+    if (e != cudaSuccess) {
+        release(v);
+        return cuda_fail(e, "cudaMemcpy(volume)");
+    }
+    rc = finish_create(v);
+    if (rc) {
+        release(v);
+        return rc;
+    }
+    *out = v;
+    return VC_OK;
+}
+
+int ensure_grad(vc_volume* v, int op, cudaStream_t s) {
+    if (v->d_grad[op]) return VC_OK;
+    float4* g = nullptr;
+    cudaError_t e = cudaMalloc(&g, (size_t)v->nx * v->ny * v->nz * sizeof(float4));
+    if (e != cudaSuccess) return fail(VC_ERR_NOMEM, std::string("cudaMalloc(gradient volume): ") + cudaGetErrorString(e));
+    e = vc::launch_gradient_prepass(v->dtype, v->d_data, v->nx, v->ny, v->nz, op, g, s);
+    if (e != cudaSuccess) {
+        cudaFree(g);
+        return cuda_fail(e, "gradient pre-pass launch");
+    }
+    v->d_grad[op] = g;
+    return VC_OK;
+}
+
+int validate_params(const vc_render_params* p, int* local_rows) {
+    if (p == nullptr) return fail(VC_ERR_INVALID, "params is null");
+    if (p->width <= 0 || p->height <= 0) return fail(VC_ERR_INVALID, "image size must be positive");
+    if (p->band_rows < 1 || p->band_step < 1 || p->band_first < 0)
+        return fail(VC_ERR_INVALID, "band_rows/band_step must be >= 1 and band_first >= 0");
+    if (p->lut_n < 1 || p->lut_n > VC_MAX_LUT) return fail(VC_ERR_INVALID, "lut_n must be in [1, VC_MAX_LUT]");
+    for (int i = 0; i + 1 < p->lut_n; i++)
+        if (!(p->lut_hu[i + 1] > p->lut_hu[i])) return fail(VC_ERR_INVALID, "transfer breakpoints must strictly increase");
+    if (p->op < 0 || p->op > 2) return fail(VC_ERR_INVALID, "op must be 0, 1 or 2");
+    if (p->interp < 0 || p->interp > 2) return fail(VC_ERR_INVALID, "interp must be 0, 1 or 2");
+    if (p->mode < 0 || p->mode > 1) return fail(VC_ERR_INVALID, "mode must be 0 or 1");
+    if (!(p->coarse > 0.0) || !(p->fine > 0.0)) return fail(VC_ERR_INVALID, "steps must be positive");
+    if (p->refine_iters < 0) return fail(VC_ERR_INVALID, "refine_iters must be >= 0");
+    if (!(p->mu_water > 0.0)) return fail(VC_ERR_INVALID, "mu_water must be positive");
+    if (p->grad_source != VC_GRAD_TAPS && p->grad_source != VC_GRAD_VOLUME)
+        return fail(VC_ERR_INVALID, "grad_source must be VC_GRAD_TAPS or VC_GRAD_VOLUME");
+    const long long nb = (p->height + p->band_rows - 1) / p->band_rows;
+    long long rows = 0;
+    for (long long b = p->band_first; b < nb; b += p->band_step)
+        rows += std::min<long long>(p->band_rows, p->height - b * p->band_rows);
+    if (rows > (1LL << 30)) return fail(VC_ERR_INVALID, "too many rows");
+    *local_rows = (int)rows;
+    return VC_OK;
+}
+
+int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64_t* d_counters,
+                cudaStream_t s, int local_rows) {
+    vc::RenderLaunch L{};
+    L.p = p;
+    L.dtype = v->dtype;
+    L.data = v->d_data;
+    L.nx = v->nx;
+    L.ny = v->ny;
+    L.nz = v->nz;
+    L.rp = make_raypos(v);
+    L.out = d_rgba;
+    L.local_rows = local_rows;
+    L.counters = d_counters;
+    L.mx = v->mx;
+    L.my = v->my;
+    L.occ = v->d_occ;
+    const bool zero_in_window = p->t_low <= 0.0 && 0.0 <= p->t_high;
+    L.skip_on = (p->skip_empty && !zero_in_window) ? 1 : 0;
+    if (L.skip_on && !(v->occ_valid && v->occ_lo == p->t_low && v->occ_hi == p->t_high)) {
+        VC_CUDA(vc::launch_occupancy(v->d_mm, v->mx * v->my * v->mz, p->t_low, p->t_high, v->d_occ, s));
+        v->occ_valid = true;
+        v->occ_lo = p->t_low;
+        v->occ_hi = p->t_high;
+    }
+    L.grad = nullptr;
+    if (p->grad_source == VC_GRAD_VOLUME) {
+        int rc = ensure_grad(v, p->op, s);
+        if (rc) return rc;
+        L.grad = v->d_grad[p->op];
+    }
+    if (d_counters) VC_CUDA(cudaMemsetAsync(d_counters, 0, VC_NUM_COUNTERS * sizeof(uint64_t), s));
+    if (local_rows == 0) return VC_OK;
+    VC_CUDA(vc::launch_raycast(L, s));
+    return VC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vc_abi_version(void) { return VC_ABI_VERSION; }
+int vc_render_params_size(void) { return (int)sizeof(vc_render_params); }
+const char* vc_last_error(void) { return g_err.c_str(); }
+
+int vc_device_count(int* out) {
+    if (!out) return fail(VC_ERR_INVALID, "out is null");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) n = 0;
+    *out = n;
+    return VC_OK;
+}
+
+int vc_volume_create(int device, const void* h_data, int dtype, int nx, int ny, int nz,
+                     const double spacing[3], vc_volume** out) {
+    return create_common(device, h_data, cudaMemcpyHostToDevice, dtype, nx, ny, nz, spacing, out);
+}
+
+int vc_volume_create_device(int device, const void* d_data, int dtype, int nx, int ny, int nz,
+                            const double spacing[3], vc_volume** out) {
+    return create_common(device, d_data, cudaMemcpyDeviceToDevice, dtype, nx, ny, nz, spacing, out);
+}
+
+int vc_volume_destroy(vc_volume* vol) {
+    release(vol);
+    return VC_OK;
+}
+
+int vc_volume_data(const vc_volume* vol, const void** d_data) {
+    if (!vol || !d_data) return fail(VC_ERR_INVALID, "null argument");
+    *d_data = vol->d_data;
+    return VC_OK;
+}
+
+int vc_gradient_prepass(vc_volume* vol, int op, void* stream) {
+    if (!vol) return fail(VC_ERR_INVALID, "volume is null");
+    if (op < 0 || op > 2) return fail(VC_ERR_INVALID, "op must be 0, 1 or 2");
+    DeviceGuard g(vol->device);
+    std::lock_guard<std::mutex> lk(vol->mu);
+    return ensure_grad(vol, op, static_cast<cudaStream_t>(stream));
+}
+
+int vc_gradient_volume(const vc_volume* vol, int op, const void** d_grad) {
+    if (!vol || !d_grad) return fail(VC_ERR_INVALID, "null argument");
+    if (op < 0 || op > 2) return fail(VC_ERR_INVALID, "op must be 0, 1 or 2");
+    *d_grad = vol->d_grad[op];
+    return VC_OK;
+}
+
+int vc_gradient_prepass_into(const vc_volume* vol, int op, void* d_out, void* stream) {
+    if (!vol || !d_out) return fail(VC_ERR_INVALID, "null argument");
+    if (op < 0 || op > 2) return fail(VC_ERR_INVALID, "op must be 0, 1 or 2");
+    DeviceGuard g(vol->device);
+    VC_CUDA(vc::launch_gradient_prepass(vol->dtype, vol->d_data, vol->nx, vol->ny, vol->nz, op,
+                                        static_cast<float4*>(d_out), static_cast<cudaStream_t>(stream)));
+    return VC_OK;
+}
+
+int vc_render(vc_volume* vol, const vc_render_params* p, uint8_t* d_rgba, uint64_t* d_counters,
+              void* stream) {
+    if (!vol) return fail(VC_ERR_INVALID, "volume is null");
+    int local_rows = 0;
+    int rc = validate_params(p, &local_rows);
+    if (rc) return rc;
+    if (!d_rgba && local_rows > 0) return fail(VC_ERR_INVALID, "output buffer is null");
+    DeviceGuard g(vol->device);
+    std::lock_guard<std::mutex> lk(vol->mu);
+    return render_impl(vol, p, d_rgba, d_counters, static_cast<cudaStream_t>(stream), local_rows);
+}
+
+int vc_render_host(vc_volume* vol, const vc_render_params* p, uint8_t* h_rgba, uint64_t* h_counters,
+                   float* ms) {
+    if (!vol) return fail(VC_ERR_INVALID, "volume is null");
+    int local_rows = 0;
+    int rc = validate_params(p, &local_rows);
+    if (rc) return rc;
+    if (!h_rgba && local_rows > 0) return fail(VC_ERR_INVALID, "output buffer is null");
+    DeviceGuard g(vol->device);
+    std::lock_guard<std::mutex> lk(vol->mu);
+    const size_t bytes = (size_t)local_rows * p->width * 4;
+    if (bytes > vol->scratch_bytes) {
+        cudaFree(vol->d_scratch);
+        vol->d_scratch = nullptr;
+        vol->scratch_bytes = 0;
+        cudaError_t e = cudaMalloc(&vol->d_scratch, bytes);
+        if (e != cudaSuccess) return fail(VC_ERR_NOMEM, std::string("cudaMalloc(frame): ") + cudaGetErrorString(e));
+        vol->scratch_bytes = bytes;
+    }
+    cudaStream_t s = vol->host_stream;
+    VC_CUDA(cudaEventRecord(vol->ev0, s));
+    rc = render_impl(vol, p, vol->d_scratch, vol->d_counters, s, local_rows);
+    if (rc) return rc;
+    if (bytes) VC_CUDA(cudaMemcpyAsync(h_rgba, vol->d_scratch, bytes, cudaMemcpyDeviceToHost, s));
+    if (h_counters)
+        VC_CUDA(cudaMemcpyAsync(h_counters, vol->d_counters, VC_NUM_COUNTERS * sizeof(uint64_t),
+                                cudaMemcpyDeviceToHost, s));
+    VC_CUDA(cudaEventRecord(vol->ev1, s));
+    VC_CUDA(cudaStreamSynchronize(s));
+    if (ms) VC_CUDA(cudaEventElapsedTime(ms, vol->ev0, vol->ev1));
+    return VC_OK;
+}
+
+// ---- point queries ------------------------------------------------------
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    ~DevBuf() { cudaFree(p); }
+};
+
+}  // namespace
+
+int vc_sample_points(const vc_volume* vol, int interp, const double* h_pts, int64_t n, double* h_out) {
+    if (!vol || (n > 0 && (!h_pts || !h_out))) return fail(VC_ERR_INVALID, "null argument");
+    if (interp < 0 || interp > 2) return fail(VC_ERR_INVALID, "interp must be 0, 1 or 2");
+    if (n <= 0) return VC_OK;
+    DeviceGuard g(vol->device);
+    DevBuf dp, dout;
+    VC_CUDA(cudaMalloc(&dp.p, n * 3 * sizeof(double)));
+    VC_CUDA(cudaMalloc(&dout.p, n * sizeof(double)));
+    VC_CUDA(cudaMemcpy(dp.p, h_pts, n * 3 * sizeof(double), cudaMemcpyHostToDevice));
+    VC_CUDA(vc::launch_sample_points(vol->dtype, vol->d_data, vol->nx, vol->ny, vol->nz, interp,
+                                     (const double*)dp.p, n, (double*)dout.p, 0));
+    VC_CUDA(cudaMemcpy(h_out, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+    return VC_OK;
+}
+
+int vc_gradient_points(const vc_volume* vol, int op, const double* h_pts, int64_t n, double* h_out) {
+    if (!vol || (n > 0 && (!h_pts || !h_out))) return fail(VC_ERR_INVALID, "null argument");
+    if (op < 0 || op > 2) return fail(VC_ERR_INVALID, "op must be 0, 1 or 2");
+    if (n <= 0) return VC_OK;
+    DeviceGuard g(vol->device);
+    DevBuf dp, dout;
+    VC_CUDA(cudaMalloc(&dp.p, n * 3 * sizeof(double)));
+    VC_CUDA(cudaMalloc(&dout.p, n * 3 * sizeof(double)));
+    VC_CUDA(cudaMemcpy(dp.p, h_pts, n * 3 * sizeof(double), cudaMemcpyHostToDevice));
+    VC_CUDA(vc::launch_gradient_points(vol->dtype, vol->d_data, vol->nx, vol->ny, vol->nz, op,
+                                       (const double*)dp.p, n, (double*)dout.p, 0));
+    VC_CUDA(cudaMemcpy(h_out, dout.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost));
+    return VC_OK;
+}
+
+int vc_box_interval_rays(const double* h_rays, int64_t n, const double lo[3], const double hi[3],
+                         double* h_out) {
+    if (n > 0 && (!h_rays || !h_out || !lo || !hi)) return fail(VC_ERR_INVALID, "null argument");
+    if (n <= 0) return VC_OK;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(VC_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+    DevBuf dr, dbox, dout;
+    double lohi[6] = {lo[0], lo[1], lo[2], hi[0], hi[1], hi[2]};
+    VC_CUDA(cudaMalloc(&dr.p, n * 6 * sizeof(double)));
+    VC_CUDA(cudaMalloc(&dbox.p, sizeof(lohi)));
+    VC_CUDA(cudaMalloc(&dout.p, n * 3 * sizeof(double)));
+    VC_CUDA(cudaMemcpy(dr.p, h_rays, n * 6 * sizeof(double), cudaMemcpyHostToDevice));
+    VC_CUDA(cudaMemcpy(dbox.p, lohi, sizeof(lohi), cudaMemcpyHostToDevice));
+    VC_CUDA(vc::launch_box_rays((const double*)dr.p, n, (const double*)dbox.p, (double*)dout.p, 0));
+    VC_CUDA(cudaMemcpy(h_out, dout.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost));
+    return VC_OK;
+}
+
+int vc_first_hit_rays(const vc_volume* vol, const double* h_rays, int64_t n, double coarse, double fine,
+                      double t_low, double t_high, int interp, double* h_out, uint64_t* h_samples) {
+    if (!vol || (n > 0 && (!h_rays || !h_out))) return fail(VC_ERR_INVALID, "null argument");
+    if (!(coarse > 0.0) || !(fine > 0.0) || fine > coarse)
+        return fail(VC_ERR_INVALID, "need 0 < fine_step <= coarse_step");
+    if (interp < 0 || interp > 2) return fail(VC_ERR_INVALID, "interp must be 0, 1 or 2");
+    if (n <= 0) return VC_OK;
+    DeviceGuard g(vol->device);
+    DevBuf dr, dout, dc;
+    VC_CUDA(cudaMalloc(&dr.p, n * 8 * sizeof(double)));
+    VC_CUDA(cudaMalloc(&dout.p, n * 4 * sizeof(double)));
+    VC_CUDA(cudaMalloc(&dc.p, sizeof(unsigned long long)));
+    VC_CUDA(cudaMemset(dc.p, 0, sizeof(unsigned long long)));
+    VC_CUDA(cudaMemcpy(dr.p, h_rays, n * 8 * sizeof(double), cudaMemcpyHostToDevice));
+    VC_CUDA(vc::launch_first_hit_rays(vol->dtype, vol->d_data, vol->nx, vol->ny, vol->nz, make_raypos(vol),
+                                      (const double*)dr.p, n, coarse, fine, t_low, t_high, interp,
+                                      (double*)dout.p, (unsigned long long*)dc.p, 0));
+    VC_CUDA(cudaMemcpy(h_out, dout.p, n * 4 * sizeof(double), cudaMemcpyDeviceToHost));
+    if (h_samples) VC_CUDA(cudaMemcpy(h_samples, dc.p, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return VC_OK;
+}
+
+int vc_bisect_rays(const vc_volume* vol, const double* h_rays, int64_t n, double t_low, double t_high,
+                   int iters, int interp, double* h_out, uint64_t* h_samples) {
+    if (!vol || (n > 0 && (!h_rays || !h_out))) return fail(VC_ERR_INVALID, "null argument");
+    if (iters < 0) return fail(VC_ERR_INVALID, "iters must be >= 0");
+    if (interp < 0 || interp > 2) return fail(VC_ERR_INVALID, "interp must be 0, 1 or 2");
+    if (n <= 0) return VC_OK;
+    DeviceGuard g(vol->device);
+    DevBuf dr, dout, dc;
+    VC_CUDA(cudaMalloc(&dr.p, n * 8 * sizeof(double)));
+    VC_CUDA(cudaMalloc(&dout.p, n * sizeof(double)));
+    VC_CUDA(cudaMalloc(&dc.p, sizeof(unsigned long long)));
+    VC_CUDA(cudaMemset(dc.p, 0, sizeof(unsigned long long)));
+    VC_CUDA(cudaMemcpy(dr.p, h_rays, n * 8 * sizeof(double), cudaMemcpyHostToDevice));
+    VC_CUDA(vc::launch_bisect_rays(vol->dtype, vol->d_data, vol->nx, vol->ny, vol->nz, make_raypos(vol),
+                                   (const double*)dr.p, n, t_low, t_high, iters, interp, (double*)dout.p,
+                                   (unsigned long long*)dc.p, 0));
+    VC_CUDA(cudaMemcpy(h_out, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+    if (h_samples) VC_CUDA(cudaMemcpy(h_samples, dc.p, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return VC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,284 @@
+// vc_device.cuh -- device-side restatement of the reference arithmetic.
+//
+// Every function mirrors one of /root/reference/pkg/src/voxelcast/_kernels.py
+// operation for operation in float64.  The translation units that include
+// this header are built with -fmad=false and the helpers below use the
+// explicit round-to-nearest intrinsics, so no multiply-add is ever
+// contracted (numba emits none either): the FP64
+// path is meant to be bit-identical to the reference.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/voxelcast_b200.h"
+
+namespace vc {
+
+// _kernels.py:25-30
+constexpr double GRAD_EPS = 1e-8;
+constexpr double OPAQUE_ALPHA = 1.0 - 1e-6;
+constexpr double MIN_REMAINING = 0.01;
+__host__ __device__ constexpr int grad_samples(int op) { return op == VC_OP_CENTRAL ? 6 : 26; }
+
+// 1/sqrt(2), 1/sqrt(3) exactly as the reference rounds them:
+// 1.0 / math.sqrt(2.0) and 1.0 / math.sqrt(3.0) (_kernels.py:173)
+constexpr double INV_SQRT2 = 0x1.6a09e667f3bccp-1;  // 0.7071067811865475
+constexpr double INV_SQRT3 = 0x1.279a74590331dp-1;  // 0.5773502691896258
+
+// ---- strict float64 helpers -----------------------------------------------
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// _kernels.py:35-37
+__device__ __forceinline__ double lerp(double f0, double f1, double t) {
+    return dadd(f0, dmul(dsub(f1, f0), t));
+}
+
+template <typename T>
+struct Vol {
+    const T* __restrict__ data;
+    int nx, ny, nz;
+};
+
+template <typename T>
+__device__ __forceinline__ T ldv(const T* p) { return __ldg(p); }
+
+// _kernels.py:40-42
+template <typename T>
+__device__ __forceinline__ double fetch(const Vol<T>& v, int i, int j, int k) {
+    uint32_t idx = ((uint32_t)k * (uint32_t)v.ny + (uint32_t)j) * (uint32_t)v.nx + (uint32_t)i;
+    return (double)ldv(v.data + idx);
+}
+
+// _kernels.py:45-49
+__device__ __forceinline__ double round_half_away(double x) {
+    if (x >= 0.0) return floor(dadd(x, 0.5));
+    return ceil(dsub(x, 0.5));
+}
+
+// _kernels.py:52-64
+__device__ __forceinline__ int cell(double v, int n, double& f) {
+    int i0 = (int)floor(v);
+    if (i0 > n - 2) i0 = n - 2;
+    if (i0 < 0) i0 = 0;
+    f = dsub(v, (double)i0);
+    return i0;
+}
+__device__ __forceinline__ int cell_hi(int i0, int n) {
+    int i1 = i0 + 1;
+    return i1 > n - 1 ? n - 1 : i1;
+}
+
+// _kernels.py:104-115
+template <typename T>
+__device__ __forceinline__ double sample_trilinear(const Vol<T>& v, double x, double y, double z) {
+    double fx, fy, fz;
+    const int i0 = cell(x, v.nx, fx), i1 = cell_hi(i0, v.nx);
+    const int j0 = cell(y, v.ny, fy), j1 = cell_hi(j0, v.ny);
+    const int k0 = cell(z, v.nz, fz), k1 = cell_hi(k0, v.nz);
+    const uint32_t sx = (uint32_t)(i1 - i0);
+    const uint32_t sy = (uint32_t)(j1 - j0) * (uint32_t)v.nx;
+    const uint32_t sz = (uint32_t)(k1 - k0) * (uint32_t)v.nx * (uint32_t)v.ny;
+    const T* b = v.data + (((uint32_t)k0 * (uint32_t)v.ny + (uint32_t)j0) * (uint32_t)v.nx + (uint32_t)i0);
+    // issue all eight gathers before any arithmetic (memory-level parallelism)
+    const T c000 = ldv(b), c100 = ldv(b + sx), c010 = ldv(b + sy), c110 = ldv(b + sy + sx);
+    const T c001 = ldv(b + sz), c101 = ldv(b + sz + sx), c011 = ldv(b + sz + sy),
+            c111 = ldv(b + sz + sy + sx);
+    const double x00 = lerp((double)c000, (double)c100, fx);
+    const double x10 = lerp((double)c010, (double)c110, fx);
+    const double x01 = lerp((double)c001, (double)c101, fx);
+    const double x11 = lerp((double)c011, (double)c111, fx);
+    const double y0 = lerp(x00, x10, fy);
+    const double y1 = lerp(x01, x11, fy);
+    return lerp(y0, y1, fz);
+}
+
+// _kernels.py:67-72
+template <typename T>
+__device__ __forceinline__ double sample_nearest(const Vol<T>& v, double x, double y, double z) {
+    return fetch(v, (int)round_half_away(x), (int)round_half_away(y), (int)round_half_away(z));
+}
+
+// _kernels.py:75-101
+template <typename T>
+__device__ double sample_linear(const Vol<T>& v, double x, double y, double z) {
+    const double fx = fabs(dsub(x, round_half_away(x)));
+    const double fy = fabs(dsub(y, round_half_away(y)));
+    const double fz = fabs(dsub(z, round_half_away(z)));
+    int axis;
+    if (fy > fx && fy >= fz) axis = 1;
+    else if (fz > fx && fz > fy) axis = 2;
+    else axis = 0;
+    double f;
+    if (axis == 0) {
+        const int j = (int)round_half_away(y), k = (int)round_half_away(z);
+        const int a0 = cell(x, v.nx, f), a1 = cell_hi(a0, v.nx);
+        return lerp(fetch(v, a0, j, k), fetch(v, a1, j, k), f);
+    }
+    if (axis == 1) {
+        const int i = (int)round_half_away(x), k = (int)round_half_away(z);
+        const int a0 = cell(y, v.ny, f), a1 = cell_hi(a0, v.ny);
+        return lerp(fetch(v, i, a0, k), fetch(v, i, a1, k), f);
+    }
+    const int i = (int)round_half_away(x), j = (int)round_half_away(y);
+    const int a0 = cell(z, v.nz, f), a1 = cell_hi(a0, v.nz);
+    return lerp(fetch(v, i, j, a0), fetch(v, i, j, a1), f);
+}
+
+template <typename T>
+__device__ __forceinline__ bool in_range(const Vol<T>& v, double x, double y, double z) {
+    return !(x < 0.0 || x > (double)(v.nx - 1) || y < 0.0 || y > (double)(v.ny - 1) || z < 0.0 ||
+             z > (double)(v.nz - 1));
+}
+
+// _kernels.py:118-127
+template <typename T, int INTERP>
+__device__ __forceinline__ double sample_any(const Vol<T>& v, double x, double y, double z) {
+    if (!in_range(v, x, y, z)) return 0.0;
+    if (INTERP == VC_TRILINEAR) return sample_trilinear(v, x, y, z);
+    if (INTERP == VC_LINEAR) return sample_linear(v, x, y, z);
+    return sample_nearest(v, x, y, z);
+}
+
+template <typename T>
+__device__ __forceinline__ double tap(const Vol<T>& v, double x, double y, double z) {
+    return sample_any<T, VC_TRILINEAR>(v, x, y, z);
+}
+
+// _kernels.py:130-137
+__host__ __device__ constexpr double smooth_weight(int u, int w) {
+    return (u == 0 && w == 0) ? 6.0 : ((u == 0 || w == 0) ? 3.0 : 1.0);
+}
+__host__ __device__ constexpr double zh_inv(int i, int j, int k) {
+    return (i * i + j * j + k * k) == 1 ? 1.0 : ((i * i + j * j + k * k) == 2 ? INV_SQRT2 : INV_SQRT3);
+}
+
+// _kernels.py:140-177 -- taps always trilinear, i->j->k accumulation order.
+// Terms whose weight is 0 add +0.0 to a sum that can never be -0.0 (it
+// starts at +0.0 and round-to-nearest never produces -0.0 from a sum
+// of non-(-0.0) operands), so they are dropped without changing a bit.
+template <typename T, int OP>
+__device__ __forceinline__ void grad_raw(const Vol<T>& v, double x, double y, double z, double g[3]) {
+    if (OP == VC_OP_CENTRAL) {
+        g[0] = dsub(tap(v, dadd(x, 1.0), y, z), tap(v, dsub(x, 1.0), y, z));
+        g[1] = dsub(tap(v, x, dadd(y, 1.0), z), tap(v, x, dsub(y, 1.0), z));
+        g[2] = dsub(tap(v, x, y, dadd(z, 1.0)), tap(v, x, y, dsub(z, 1.0)));
+        return;
+    }
+    double gx = 0.0, gy = 0.0, gz = 0.0;
+#pragma unroll
+    for (int i = -1; i < 2; i++) {
+#pragma unroll
+        for (int j = -1; j < 2; j++) {
+#pragma unroll
+            for (int k = -1; k < 2; k++) {
+                if (i == 0 && j == 0 && k == 0) continue;
+                const double s = tap(v, dadd(x, (double)i), dadd(y, (double)j), dadd(z, (double)k));
+                double wx, wy, wz;
+                if (OP == VC_OP_SOBEL3D) {
+                    wx = (double)i * smooth_weight(j, k);
+                    wy = (double)j * smooth_weight(i, k);
+                    wz = (double)k * smooth_weight(i, j);
+                } else {
+                    const double inv = zh_inv(i, j, k);
+                    wx = (double)i * inv;
+                    wy = (double)j * inv;
+                    wz = (double)k * inv;
+                }
+                if (i != 0) gx = dadd(gx, dmul(wx, s));
+                if (j != 0) gy = dadd(gy, dmul(wy, s));
+                if (k != 0) gz = dadd(gz, dmul(wz, s));
+            }
+        }
+    }
+    g[0] = gx;
+    g[1] = gy;
+    g[2] = gz;
+}
+
+// _kernels.py:180-185
+__device__ __forceinline__ void normalize3(const double g[3], double u[3]) {
+    const double n = __dsqrt_rn(dadd(dadd(dmul(g[0], g[0]), dmul(g[1], g[1])), dmul(g[2], g[2])));
+    if (n <= GRAD_EPS) {
+        u[0] = u[1] = u[2] = 0.0;
+        return;
+    }
+    u[0] = ddiv(g[0], n);
+    u[1] = ddiv(g[1], n);
+    u[2] = ddiv(g[2], n);
+}
+
+// _kernels.py:188-224 (slab_interval + box_interval)
+__device__ __forceinline__ bool box_interval(const double o[3], const double d[3], const double lo[3],
+                                             const double hi[3], double& t0, double& t1) {
+    double tmin = -1e300, tmax = 1e300;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        if (d[a] == 0.0) {
+            if (o[a] < lo[a] || o[a] > hi[a]) return false;
+        } else {
+            const double inv = ddiv(1.0, d[a]);
+            double ta = dmul(dsub(lo[a], o[a]), inv);
+            double tb = dmul(dsub(hi[a], o[a]), inv);
+            if (ta > tb) {
+                const double s = ta;
+                ta = tb;
+                tb = s;
+            }
+            if (ta > tmin) tmin = ta;
+            if (tb < tmax) tmax = tb;
+        }
+    }
+    if (tmin > tmax) return false;
+    if (tmax < 0.0) return false;
+    t0 = tmin < 0.0 ? 0.0 : tmin;
+    t1 = tmax;
+    return true;
+}
+
+// Ray-to-voxel-space position, _kernels.py:414-416: (o + t*d)/s - 0.5.
+// When every spacing is a power of two the division is exact as a
+// multiply by the (exact) reciprocal, so UNIT/POW2 spacing takes the fast
+// form without changing a bit.
+struct RayPos {
+    double o[3], d[3], s[3], rs[3];
+    bool pow2;
+    __device__ __forceinline__ void at(double t, double p[3]) const {
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            const double w = dadd(o[a], dmul(t, d[a]));
+            p[a] = dsub(pow2 ? dmul(w, rs[a]) : ddiv(w, s[a]), 0.5);
+        }
+    }
+};
+
+// _kernels.py:514-525
+__device__ __forceinline__ double clamp01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
+__device__ __forceinline__ uint8_t quant(double v) {
+    return (uint8_t)(int)dadd(dmul(clamp01(v), 255.0), 0.5);
+}
+
+// _kernels.py:490-511; breakpoints read from the kernel-parameter bank
+__device__ __forceinline__ void lut_eval(const vc_render_params& P, double hu, double out[4]) {
+    const int n = P.lut_n;
+    if (hu <= P.lut_hu[0]) {
+#pragma unroll
+        for (int c = 0; c < 4; c++) out[c] = P.lut_rgba[0][c];
+        return;
+    }
+    if (hu >= P.lut_hu[n - 1]) {
+#pragma unroll
+        for (int c = 0; c < 4; c++) out[c] = P.lut_rgba[n - 1][c];
+        return;
+    }
+    int i = 0;
+    while (i + 1 < n - 1 && P.lut_hu[i + 1] <= hu) i++;
+    const double t = ddiv(dsub(hu, P.lut_hu[i]), dsub(P.lut_hu[i + 1], P.lut_hu[i]));
+#pragma unroll
+    for (int c = 0; c < 4; c++) out[c] = lerp(P.lut_rgba[i][c], P.lut_rgba[i + 1][c], t);
+}
+
+}  // namespace vc

@@ -1,0 +1,54 @@
+// vc_internal.h -- launchers shared between the C-ABI layer and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "vc_device.cuh"
+
+namespace vc {
+
+struct RenderLaunch {
+    const vc_render_params* p;
+    int dtype;
+    const void* data;
+    int nx, ny, nz;
+    const void* grad;     // packed float4 gradient volume or nullptr (taps)
+    RayPos rp;            // spacing / reciprocal / pow2 filled in; o, d per pixel
+    const uint8_t* occ;   // macrocell occupancy for the current window
+    int mx, my;
+    int skip_on;
+    uint8_t* out;         // local_rows x width x 4
+    int local_rows;
+    uint64_t* counters;   // VC_NUM_COUNTERS or nullptr
+};
+
+cudaError_t launch_raycast(const RenderLaunch& L, cudaStream_t s);
+
+// Kernel 1 (gradient_prepass.cu)
+cudaError_t launch_gradient_prepass(int dtype, const void* data, int nx, int ny, int nz, int op,
+                                    float4* out, cudaStream_t s);
+
+// macrocells (macrocell.cu)
+cudaError_t launch_macrocell_minmax(int dtype, const void* data, int nx, int ny, int nz, float2* mm,
+                                    int mx, int my, int mz, cudaStream_t s);
+cudaError_t launch_occupancy(const float2* mm, int count, double lo, double hi, uint8_t* occ,
+                             cudaStream_t s);
+
+// point queries (points.cu)
+cudaError_t launch_sample_points(int dtype, const void* data, int nx, int ny, int nz, int interp,
+                                 const double* pts, int64_t n, double* out, cudaStream_t s);
+cudaError_t launch_gradient_points(int dtype, const void* data, int nx, int ny, int nz, int op,
+                                   const double* pts, int64_t n, double* out, cudaStream_t s);
+cudaError_t launch_box_rays(const double* rays, int64_t n, const double* lohi, double* out,
+                            cudaStream_t s);
+cudaError_t launch_first_hit_rays(int dtype, const void* data, int nx, int ny, int nz, RayPos rp,
+                                  const double* rays, int64_t n, double coarse, double fine,
+                                  double t_low, double t_high, int interp, double* out,
+                                  unsigned long long* samples, cudaStream_t s);
+cudaError_t launch_bisect_rays(int dtype, const void* data, int nx, int ny, int nz, RayPos rp,
+                               const double* rays, int64_t n, double t_low, double t_high, int iters,
+                               int interp, double* out, unsigned long long* samples, cudaStream_t s);
+
+}  // namespace vc

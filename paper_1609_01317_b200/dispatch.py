@@ -1,0 +1,107 @@
+"""Image-tile multi-GPU dispatcher (new subsystem; the reference renders on
+one host's thread pool, raycast.py:476-505).
+
+One process per GPU (torchrun), the volume replicated on every GPU.  Each
+frame is cut into bands of `band_rows` rows; band b belongs to rank
+b % world (interleaved, so every rank gets a similar mix of empty sky,
+surface hits and translucent paths -- SURVEY.md §8(e) measured 1.05-1.17
+max/mean imbalance for contiguous bands at 8 ranks).  A rank renders its
+bands packed into one buffer with a single kernel launch (vc_render with
+band_first = rank, band_step = world), the packed buffers are exchanged
+with one NCCL all-gather over NVLink, and a device gather puts rows back in
+image order.  Pixels are independent, so the assembled frame is
+bit-identical to the single-GPU frame (pkg/tests/test_render.py:111-122).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .raycast import FrameBuffer, RenderSettings, Scene, render_params, sample_count_of
+from .volume import Volume, device_volume
+
+
+@dataclass
+class BandPlan:
+    height: int
+    width: int
+    band_rows: int
+    world: int
+    rank: int
+
+    def __post_init__(self):
+        if self.band_rows < 1 or self.world < 1 or not 0 <= self.rank < self.world:
+            raise ValueError("band_rows >= 1, world >= 1 and 0 <= rank < world required")
+        nb = -(-self.height // self.band_rows)
+        self.rows_of = []
+        for r in range(self.world):
+            rows = [y for b in range(r, nb, self.world)
+                    for y in range(b * self.band_rows, min((b + 1) * self.band_rows, self.height))]
+            self.rows_of.append(np.array(rows, np.int64))
+        self.local_rows = len(self.rows_of[self.rank])
+        self.max_rows = max(len(r) for r in self.rows_of)
+        # image row y comes from packed row src[y] of the (world * max_rows) gather buffer
+        src = np.empty(self.height, np.int64)
+        for r, rows in enumerate(self.rows_of):
+            src[rows] = r * self.max_rows + np.arange(len(rows))
+        self.src = src
+
+
+class TileGather:
+    """NCCL all-gather of packed bands + device unpermute to image order."""
+
+    def __init__(self, plan: BandPlan, device, group=None):
+        import torch
+
+        self.plan = plan
+        self.group = group
+        self.device = torch.device(device)
+        self.send = torch.empty((plan.max_rows, plan.width, 4), dtype=torch.uint8, device=self.device)
+        self.recv = torch.empty((plan.world * plan.max_rows, plan.width, 4), dtype=torch.uint8,
+                                device=self.device)
+        self.src = torch.as_tensor(plan.src, device=self.device)
+
+    def __call__(self, local):
+        import torch
+        import torch.distributed as dist
+
+        n = self.plan.local_rows
+        if n:
+            self.send[:n].copy_(local[:n], non_blocking=True)
+        dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+        return torch.index_select(self.recv, 0, self.src)
+
+
+def render_frame_distributed(volume: Volume, scene: Scene, settings: RenderSettings | None = None,
+                             *, band_rows: int = 8, group=None) -> FrameBuffer | None:
+    """render_frame across all ranks of the default process group (one GPU
+    per rank, LOCAL_RANK = device).  Every rank gets the full frame back."""
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    settings = settings or RenderSettings()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = torch.cuda.current_device()
+    plan = BandPlan(settings.height, settings.width, band_rows, world, rank)
+    dv = device_volume(volume, dev)
+    P = render_params(volume, scene, settings, band_rows=band_rows, band_first=rank, band_step=world)
+    local = torch.empty((max(plan.local_rows, 1), settings.width, 4), dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(_native.NUM_COUNTERS, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    t0 = time.perf_counter()
+    _native.check(_native.load().vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(local.data_ptr()),
+                                           ctypes.c_void_p(cnt.data_ptr()),
+                                           ctypes.c_void_p(stream.cuda_stream)))
+    img = TileGather(plan, dev, group)(local) if world > 1 else local[: settings.height]
+    dist.all_reduce(cnt, group=group)
+    pixels = img.cpu().numpy()
+    ms = (time.perf_counter() - t0) * 1000.0
+    c = cnt.cpu().numpy()
+    return FrameBuffer(settings.width, settings.height, pixels, ms, sample_count_of(c, P.op))

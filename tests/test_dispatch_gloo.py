@@ -1,0 +1,78 @@
+"""Multi-process (gloo, world_size 2, CPU) coverage of the image-tile
+dispatcher's host logic: band ownership, packing, all-gather and the
+unpermute back to image order."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1609_01317_b200.dispatch import BandPlan, TileGather
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def fake_band_render(plan: BandPlan) -> torch.Tensor:
+    """Stand-in for vc_render: fills each local row with its global row id."""
+    rows = plan.rows_of[plan.rank]
+    out = torch.zeros((max(plan.local_rows, 1), plan.width, 4), dtype=torch.uint8)
+    for i, y in enumerate(rows):
+        out[i, :, 0] = y % 251
+        out[i, :, 1] = (y // 251) % 251
+        out[i, :, 2] = torch.arange(plan.width) % 256
+        out[i, :, 3] = 255
+    return out
+
+
+def _worker(rank, world, port, cases, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        for (H, W, band) in cases:
+            plan = BandPlan(H, W, band, world, rank)
+            img = TileGather(plan, "cpu")(fake_band_render(plan)).numpy()
+            y = np.arange(H)
+            ok = (np.array_equal(img[:, 0, 0], y % 251) and np.array_equal(img[:, 0, 1], (y // 251) % 251)
+                  and (img[:, :, 3] == 255).all())
+            q.put((rank, H, W, band, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_tile_gather_reassembles_image(world):
+    cases = [(1080, 24, 8), (37, 5, 4), (9, 3, 16), (100, 2, 1)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    results = [q.get(timeout=5) for _ in range(world * len(cases))]
+    assert all(r[-1] for r in results), results
+
+
+def test_band_plan_covers_every_row_once():
+    for H, band, world in [(1080, 8, 8), (1080, 8, 3), (7, 16, 4), (2160, 8, 5)]:
+        seen = np.concatenate([BandPlan(H, 4, band, world, r).rows_of[r] for r in range(world)])
+        assert np.array_equal(np.sort(seen), np.arange(H))
+        plan = BandPlan(H, 4, band, world, 0)
+        assert sorted(plan.src.tolist()) == sorted(
+            r * plan.max_rows + i for r in range(world) for i in range(len(plan.rows_of[r])))
+    with pytest.raises(ValueError):
+        BandPlan(10, 4, 0, 2, 0)
