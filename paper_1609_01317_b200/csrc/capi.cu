@@ -27,7 +27,8 @@ struct vc_volume {
     void* d_data = nullptr;
     size_t bytes = 0;
     float2* d_mm = nullptr;
-    uint8_t* d_occ = nullptr;
+    uint8_t* d_occ = nullptr;      // macrocell distance field of the last window
+    uint8_t* d_occ_tmp = nullptr;
     int mx = 0, my = 0, mz = 0;
     bool occ_valid = false;
     double occ_lo = 0.0, occ_hi = 0.0;
@@ -113,6 +114,7 @@ int finish_create(vc_volume* v) {
     const size_t mc = (size_t)v->mx * v->my * v->mz;
     VC_CUDA(cudaMalloc(&v->d_mm, mc * sizeof(float2)));
     VC_CUDA(cudaMalloc(&v->d_occ, mc));
+    VC_CUDA(cudaMalloc(&v->d_occ_tmp, mc));
     VC_CUDA(cudaMalloc(&v->d_counters, VC_NUM_COUNTERS * sizeof(uint64_t)));
     VC_CUDA(cudaStreamCreateWithFlags(&v->host_stream, cudaStreamNonBlocking));
     VC_CUDA(cudaEventCreate(&v->ev0));
@@ -129,6 +131,7 @@ void release(vc_volume* v) {
     cudaFree(v->d_data);
     cudaFree(v->d_mm);
     cudaFree(v->d_occ);
+    cudaFree(v->d_occ_tmp);
     for (auto& p : v->d_grad) cudaFree(p);
     cudaFree(v->d_scratch);
     cudaFree(v->d_counters);
@@ -235,7 +238,8 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
     const bool zero_in_window = p->t_low <= 0.0 && 0.0 <= p->t_high;
     L.skip_on = (p->skip_empty && !zero_in_window) ? 1 : 0;
     if (L.skip_on && !(v->occ_valid && v->occ_lo == p->t_low && v->occ_hi == p->t_high)) {
-        VC_CUDA(vc::launch_occupancy(v->d_mm, v->mx * v->my * v->mz, p->t_low, p->t_high, v->d_occ, s));
+        VC_CUDA(vc::launch_occupancy(v->d_mm, v->mx, v->my, v->mz, p->t_low, p->t_high, v->d_occ,
+                                     v->d_occ_tmp, s));
         v->occ_valid = true;
         v->occ_lo = p->t_low;
         v->occ_hi = p->t_high;

@@ -42,11 +42,49 @@ __global__ void macrocell_minmax_kernel(const T* __restrict__ vol, int nx, int n
     }
 }
 
+// occupancy of the window [lo, hi]: 0 = may hold an in-window sample,
+// DIST_CAP = empty.  Empty cells start at the cap, not at infinity: after
+// DIST_PASSES relaxation passes every cell within DIST_PASSES of an
+// occupied one holds its exact distance, and every other cell keeps
+// DIST_CAP = DIST_PASSES + 1, a valid lower bound of its distance.
+constexpr uint8_t DIST_CAP = DIST_PASSES + 1;
+
 __global__ void occupancy_kernel(const float2* __restrict__ mm, int count, double lo, double hi,
-                                 uint8_t* occ) {
+                                 uint8_t* dist) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
         const float2 r = mm[i];
-        occ[i] = ((double)r.x <= hi && (double)r.y >= lo) ? 1 : 0;
+        dist[i] = ((double)r.x <= hi && (double)r.y >= lo) ? 0 : DIST_CAP;
+    }
+}
+
+// One relaxation pass of the Chebyshev (L-infinity) distance transform of
+// the occupancy over the 26-neighbourhood.  Macrocells outside the grid
+// hold no in-range sample and count as empty.  Shortest 26-neighbour paths
+// have exactly the Chebyshev length, so dist[m] = d >= 1 guarantees that
+// every macrocell within Chebyshev distance d - 1 of m is empty.
+__global__ void chebyshev_pass_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int mx,
+                                      int my, int mz) {
+    const int count = mx * my * mz;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+        const int x = i % mx, y = (i / mx) % my, z = i / (mx * my);
+        int best = in[i];
+        if (best != 0) {
+            for (int dz = -1; dz <= 1; dz++) {
+                const int zz = z + dz;
+                if (zz < 0 || zz >= mz) continue;
+                for (int dy = -1; dy <= 1; dy++) {
+                    const int yy = y + dy;
+                    if (yy < 0 || yy >= my) continue;
+                    for (int dx = -1; dx <= 1; dx++) {
+                        const int xx = x + dx;
+                        if (xx < 0 || xx >= mx) continue;
+                        const int v = in[(zz * my + yy) * mx + xx] + 1;
+                        if (v < best) best = v;
+                    }
+                }
+            }
+        }
+        out[i] = (uint8_t)best;
     }
 }
 
@@ -72,12 +110,19 @@ cudaError_t launch_macrocell_minmax(int dtype, const void* data, int nx, int ny,
     return cudaGetLastError();
 }
 
-cudaError_t launch_occupancy(const float2* mm, int count, double lo, double hi, uint8_t* occ,
-                             cudaStream_t s) {
+cudaError_t launch_occupancy(const float2* mm, int mx, int my, int mz, double lo, double hi, uint8_t* dist,
+                             uint8_t* scratch, cudaStream_t s) {
+    const int count = mx * my * mz;
     int blocks = (count + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
-    occupancy_kernel<<<blocks, 256, 0, s>>>(mm, count, lo, hi, occ);
+    occupancy_kernel<<<blocks, 256, 0, s>>>(mm, count, lo, hi, dist);
+    // distances up to DIST_PASSES + 1 macrocells (8 voxels each); an even
+    // pass count leaves the result in `dist`
+    for (int p = 0; p < DIST_PASSES; p += 2) {
+        chebyshev_pass_kernel<<<blocks, 256, 0, s>>>(dist, scratch, mx, my, mz);
+        chebyshev_pass_kernel<<<blocks, 256, 0, s>>>(scratch, dist, mx, my, mz);
+    }
     return cudaGetLastError();
 }
 

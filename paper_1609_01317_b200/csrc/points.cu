@@ -136,7 +136,7 @@ cudaError_t launch_sample_points(int dtype, const void* data, int nx, int ny, in
                                  const double* pts, int64_t n, double* out, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     VC_DISPATCH_DTYPE(dtype, T, {
-        Vol<T> v{static_cast<const T*>(data), nx, ny, nz};
+        const Vol<T> v = make_vol(static_cast<const T*>(data), nx, ny, nz);
         if (interp == VC_NEAREST)
             sample_points_kernel<T, VC_NEAREST><<<blocks_for(n), 128, 0, s>>>(v, pts, n, out);
         else if (interp == VC_LINEAR)
@@ -151,7 +151,7 @@ cudaError_t launch_gradient_points(int dtype, const void* data, int nx, int ny, 
                                    const double* pts, int64_t n, double* out, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     VC_DISPATCH_DTYPE(dtype, T, {
-        Vol<T> v{static_cast<const T*>(data), nx, ny, nz};
+        const Vol<T> v = make_vol(static_cast<const T*>(data), nx, ny, nz);
         if (op == VC_OP_CENTRAL)
             gradient_points_kernel<T, VC_OP_CENTRAL><<<blocks_for(n), 128, 0, s>>>(v, pts, n, out);
         else if (op == VC_OP_SOBEL3D)
@@ -175,7 +175,7 @@ cudaError_t launch_first_hit_rays(int dtype, const void* data, int nx, int ny, i
                                   unsigned long long* samples, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     VC_DISPATCH_DTYPE(dtype, T, {
-        Vol<T> v{static_cast<const T*>(data), nx, ny, nz};
+        const Vol<T> v = make_vol(static_cast<const T*>(data), nx, ny, nz);
         if (interp == VC_NEAREST)
             first_hit_kernel<T, VC_NEAREST><<<blocks_for(n), 128, 0, s>>>(v, rp, rays, n, coarse, fine,
                                                                         t_low, t_high, out, samples);
@@ -194,7 +194,7 @@ cudaError_t launch_bisect_rays(int dtype, const void* data, int nx, int ny, int 
                                int interp, double* out, unsigned long long* samples, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     VC_DISPATCH_DTYPE(dtype, T, {
-        Vol<T> v{static_cast<const T*>(data), nx, ny, nz};
+        const Vol<T> v = make_vol(static_cast<const T*>(data), nx, ny, nz);
         if (interp == VC_NEAREST)
             bisect_kernel<T, VC_NEAREST><<<blocks_for(n), 128, 0, s>>>(v, rp, rays, n, t_low, t_high,
                                                                      iters, out, samples);

@@ -41,7 +41,26 @@ template <typename T>
 struct Vol {
     const T* __restrict__ data;
     int nx, ny, nz;
+    // n-1 and max(n-2, 0) as doubles: range checks and cell clamps without
+    // an I2F.F64 per sample (make_vol fills them)
+    double mx, my, mz, cx, cy, cz;
 };
+
+template <typename T>
+__host__ __device__ inline Vol<T> make_vol(const T* data, int nx, int ny, int nz) {
+    Vol<T> v;
+    v.data = data;
+    v.nx = nx;
+    v.ny = ny;
+    v.nz = nz;
+    v.mx = (double)(nx - 1);
+    v.my = (double)(ny - 1);
+    v.mz = (double)(nz - 1);
+    v.cx = (double)(nx - 2 < 0 ? 0 : nx - 2);
+    v.cy = (double)(ny - 2 < 0 ? 0 : ny - 2);
+    v.cz = (double)(nz - 2 < 0 ? 0 : nz - 2);
+    return v;
+}
 
 template <typename T>
 __device__ __forceinline__ T ldv(const T* p) { return __ldg(p); }
@@ -59,12 +78,44 @@ __device__ __forceinline__ double round_half_away(double x) {
     return ceil(dsub(x, 0.5));
 }
 
-// _kernels.py:52-64
-__device__ __forceinline__ int cell(double v, int n, double& f) {
-    int i0 = (int)floor(v);
-    if (i0 > n - 2) i0 = n - 2;
-    if (i0 < 0) i0 = 0;
-    f = dsub(v, (double)i0);
+// ---- conversion-free integer <-> float64 helpers ---------------------------
+// On sm_100 the float64 conversions (I2F.F64, F2I.F64.FLOOR, F2F.F64.F32)
+// issue on the narrow XU pipe, which the first profile showed saturated
+// (profiles/r01_*).  These replacements run on the FP64 / integer pipes and
+// are exact: 2^52 + v is representable for every 0 <= v < 2^32.
+constexpr double TWO52 = 0x1p52;
+constexpr double TWO52_31 = 0x1.000008p52;  // 2^52 + 2^31
+
+// exact double of an unsigned 32-bit integer
+__device__ __forceinline__ double u2d(uint32_t v) { return __dsub_rn(__hiloint2double(0x43300000, (int)v), TWO52); }
+// exact double of a signed integer d, given biased = d + 2^31 (mod 2^32)
+__device__ __forceinline__ double biased2d(uint32_t biased) {
+    return __dsub_rn(__hiloint2double(0x43300000, (int)biased), TWO52_31);
+}
+
+// floor(x) for 0 <= x < 2^31: returns the integer, r = (double)floor(x)
+__device__ __forceinline__ int floor_pos(double x, double& r) {
+    const double t = __dadd_rn(x, TWO52);  // round-to-nearest-even integer
+    int i = __double2loint(t);
+    r = __dsub_rn(t, TWO52);
+    if (r > x) {
+        r = __dsub_rn(r, 1.0);
+        i -= 1;
+    }
+    return i;
+}
+
+// _kernels.py:52-64 for an in-range coordinate 0 <= v <= n-1: lower cell
+// corner clamped to n-2 (and to 0 when n == 1), fraction f = v - i0.
+// nm2 = (double)max(n-2, 0).
+__device__ __forceinline__ int cell(double v, int n, double nm2, double& f) {
+    double r;
+    int i0 = floor_pos(v, r);
+    if (i0 > n - 2) {
+        i0 = n - 2 < 0 ? 0 : n - 2;
+        r = nm2;
+    }
+    f = dsub(v, r);
     return i0;
 }
 __device__ __forceinline__ int cell_hi(int i0, int n) {
@@ -72,25 +123,54 @@ __device__ __forceinline__ int cell_hi(int i0, int n) {
     return i1 > n - 1 ? n - 1 : i1;
 }
 
-// _kernels.py:104-115
+template <typename T>
+struct VoxelBits;  // raw voxel -> exact double, and lerp over a voxel pair
+template <>
+struct VoxelBits<uint8_t> {
+    static constexpr bool integral = true;
+};
+template <>
+struct VoxelBits<uint16_t> {
+    static constexpr bool integral = true;
+};
+template <>
+struct VoxelBits<float> {
+    static constexpr bool integral = false;
+};
+
+// lerp(c0, c1, t) = c0 + (c1 - c0) * t over two voxel values, bit-identical
+// to the reference's float64 expression (c1 - c0 is exact for integer data).
+template <typename T>
+__device__ __forceinline__ double lerp_vox(T c0, T c1, double t) {
+    if constexpr (VoxelBits<T>::integral) {
+        const double f0 = u2d((uint32_t)c0);
+        const double d = biased2d((uint32_t)c1 - (uint32_t)c0 + 0x80000000u);
+        return dadd(f0, dmul(d, t));
+    } else {
+        return lerp((double)c0, (double)c1, t);
+    }
+}
+
+// _kernels.py:104-115 for an in-range position (sample_any checked it).
+// All eight gathers are issued before any arithmetic (memory-level
+// parallelism); offsets are 32-bit from the cell's base corner.
 template <typename T>
 __device__ __forceinline__ double sample_trilinear(const Vol<T>& v, double x, double y, double z) {
     double fx, fy, fz;
-    const int i0 = cell(x, v.nx, fx), i1 = cell_hi(i0, v.nx);
-    const int j0 = cell(y, v.ny, fy), j1 = cell_hi(j0, v.ny);
-    const int k0 = cell(z, v.nz, fz), k1 = cell_hi(k0, v.nz);
+    const int i0 = cell(x, v.nx, v.cx, fx), i1 = cell_hi(i0, v.nx);
+    const int j0 = cell(y, v.ny, v.cy, fy), j1 = cell_hi(j0, v.ny);
+    const int k0 = cell(z, v.nz, v.cz, fz), k1 = cell_hi(k0, v.nz);
     const uint32_t sx = (uint32_t)(i1 - i0);
     const uint32_t sy = (uint32_t)(j1 - j0) * (uint32_t)v.nx;
     const uint32_t sz = (uint32_t)(k1 - k0) * (uint32_t)v.nx * (uint32_t)v.ny;
     const T* b = v.data + (((uint32_t)k0 * (uint32_t)v.ny + (uint32_t)j0) * (uint32_t)v.nx + (uint32_t)i0);
-    // issue all eight gathers before any arithmetic (memory-level parallelism)
     const T c000 = ldv(b), c100 = ldv(b + sx), c010 = ldv(b + sy), c110 = ldv(b + sy + sx);
     const T c001 = ldv(b + sz), c101 = ldv(b + sz + sx), c011 = ldv(b + sz + sy),
             c111 = ldv(b + sz + sy + sx);
-    const double x00 = lerp((double)c000, (double)c100, fx);
-    const double x10 = lerp((double)c010, (double)c110, fx);
-    const double x01 = lerp((double)c001, (double)c101, fx);
-    const double x11 = lerp((double)c011, (double)c111, fx);
+    const double x00 = lerp_vox<T>(c000, c100, fx);
+    const double x10 = lerp_vox<T>(c010, c110, fx);
+    const double x01 = lerp_vox<T>(c001, c101, fx);
+    const double x11 = lerp_vox<T>(c011, c111, fx);
     const double y0 = lerp(x00, x10, fy);
     const double y1 = lerp(x01, x11, fy);
     return lerp(y0, y1, fz);
@@ -115,23 +195,22 @@ __device__ double sample_linear(const Vol<T>& v, double x, double y, double z) {
     double f;
     if (axis == 0) {
         const int j = (int)round_half_away(y), k = (int)round_half_away(z);
-        const int a0 = cell(x, v.nx, f), a1 = cell_hi(a0, v.nx);
+        const int a0 = cell(x, v.nx, v.cx, f), a1 = cell_hi(a0, v.nx);
         return lerp(fetch(v, a0, j, k), fetch(v, a1, j, k), f);
     }
     if (axis == 1) {
         const int i = (int)round_half_away(x), k = (int)round_half_away(z);
-        const int a0 = cell(y, v.ny, f), a1 = cell_hi(a0, v.ny);
+        const int a0 = cell(y, v.ny, v.cy, f), a1 = cell_hi(a0, v.ny);
         return lerp(fetch(v, i, a0, k), fetch(v, i, a1, k), f);
     }
     const int i = (int)round_half_away(x), j = (int)round_half_away(y);
-    const int a0 = cell(z, v.nz, f), a1 = cell_hi(a0, v.nz);
+    const int a0 = cell(z, v.nz, v.cz, f), a1 = cell_hi(a0, v.nz);
     return lerp(fetch(v, i, j, a0), fetch(v, i, j, a1), f);
 }
 
 template <typename T>
 __device__ __forceinline__ bool in_range(const Vol<T>& v, double x, double y, double z) {
-    return !(x < 0.0 || x > (double)(v.nx - 1) || y < 0.0 || y > (double)(v.ny - 1) || z < 0.0 ||
-             z > (double)(v.nz - 1));
+    return !(x < 0.0 || x > v.mx || y < 0.0 || y > v.my || z < 0.0 || z > v.mz);
 }
 
 // _kernels.py:118-127

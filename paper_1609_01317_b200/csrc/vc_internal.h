@@ -33,8 +33,10 @@ cudaError_t launch_gradient_prepass(int dtype, const void* data, int nx, int ny,
 // macrocells (macrocell.cu)
 cudaError_t launch_macrocell_minmax(int dtype, const void* data, int nx, int ny, int nz, float2* mm,
                                     int mx, int my, int mz, cudaStream_t s);
-cudaError_t launch_occupancy(const float2* mm, int count, double lo, double hi, uint8_t* occ,
-                             cudaStream_t s);
+// occupancy of [lo, hi] + its Chebyshev distance field (dist: 0 = occupied)
+constexpr int DIST_PASSES = 16;
+cudaError_t launch_occupancy(const float2* mm, int mx, int my, int mz, double lo, double hi, uint8_t* dist,
+                             uint8_t* scratch, cudaStream_t s);
 
 // point queries (points.cu)
 cudaError_t launch_sample_points(int dtype, const void* data, int nx, int ny, int nz, int interp,

@@ -84,22 +84,37 @@ def ct_phantom(n: int = 512, skull_hu: float = 300.0) -> Volume:
     (SURVEY.md §8(d), C3)."""
     c = _centers(n)
     out = np.empty((n, n, n), np.uint16)
-    y = c[:, None]
-    x = c[None, :]
+    h = 2.0 / n
+    boxes = []  # conservative voxel-index bounding box of each ellipsoid
+    for (a, b, cc, x0, y0, z0, phi, dens) in SHEPP_LOGAN_3D:
+        ph = math.radians(phi)
+        ex = math.sqrt((a * math.cos(ph)) ** 2 + (b * math.sin(ph)) ** 2)
+        ey = math.sqrt((a * math.sin(ph)) ** 2 + (b * math.cos(ph)) ** 2)
+        box = []
+        for lo, hi in ((x0 - ex, x0 + ex), (y0 - ey, y0 + ey), (z0 - cc, z0 + cc)):
+            i0 = max(int(math.floor((lo + 1.0) / h - 0.5)) - 1, 0)
+            i1 = min(int(math.ceil((hi + 1.0) / h - 0.5)) + 2, n)
+            box.append((i0, i1))
+        boxes.append(box)
     for kz in range(n):  # slice by slice keeps peak memory at O(n^2)
         z = c[kz]
         v = np.zeros((n, n), np.float64)
         head = np.zeros((n, n), bool)
         for idx, (a, b, cc, x0, y0, z0, phi, dens) in enumerate(SHEPP_LOGAN_3D):
+            (xa, xb), (ya, yb), (za, zb) = boxes[idx]
+            if not za <= kz < zb or xa >= xb or ya >= yb:
+                continue
             ph = math.radians(phi)
             cp, sp = math.cos(ph), math.sin(ph)
+            y = c[ya:yb, None]
+            x = c[None, xa:xb]
             dx, dy, dz = x - x0, y - y0, z - z0
             xr = dx * cp + dy * sp
             yr = -dx * sp + dy * cp
             inside = (xr / a) ** 2 + (yr / b) ** 2 + (dz / cc) ** 2 <= 1.0
-            v = v + np.where(inside, dens, 0.0)
+            v[ya:yb, xa:xb] += np.where(inside, dens, 0.0)
             if idx == 0:
-                head = inside
+                head[ya:yb, xa:xb] = inside
         raw = 1000.0 + (v - 0.2) / 0.8 * skull_hu
         raw = np.where(head, np.clip(np.rint(raw), 0, 4095), 0.0)
         out[kz] = raw.astype(np.uint16)
