@@ -8,12 +8,14 @@ CUDA device is visible, every compute call raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 import numpy as np
 
-_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libvoxelcast_b200.so"
+# VC_LIB overrides the library path (development variants, tools/kbench.py)
+_LIB_PATH = Path(os.environ.get("VC_LIB") or Path(__file__).resolve().parent / "_lib" / "libvoxelcast_b200.so")
 
 VC_OK = 0
 VC_ERR_INVALID = 1

@@ -38,17 +38,23 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    OUT_DIR.mkdir(exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines: list[str] | None = None,
+          tag: str | None = None) -> Path:
+    """Compile (incrementally) into _lib/.  `defines` / `tag` build a
+    development variant into _lib/<tag>/ without touching the main library."""
+    out_dir = OUT_DIR if tag is None else OUT_DIR / tag
+    out_dir.mkdir(parents=True, exist_ok=True)
+    lib = out_dir / LIB.name
+    extra = [f"-D{d}" for d in (defines or [])]
     hdrs = [CSRC / h for h in HEADERS] + [ROOT / "include" / "voxelcast_b200.h"]
     objs = []
     jobs = []
     for src in SOURCES:
         s = CSRC / src
-        o = OUT_DIR / (s.stem + ".o")
+        o = out_dir / (s.stem + ".o")
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", str(s), "-o", str(o)]
+            cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", str(s), "-o", str(o)]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
             jobs.append(cmd)
@@ -63,12 +69,14 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         for log in ex.map(run, jobs):
             if verbose and log:
                 sys.stderr.write(log)
-    if force or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *map(str, objs), "-o", str(LIB)]
+    if force or _stale(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *map(str, objs), "-o", str(lib)]
         run(cmd)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    tags = [a[6:] for a in sys.argv[1:] if a.startswith("--tag=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs,
+                tag=tags[0] if tags else None))

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "vc_internal.h"
 
@@ -36,6 +37,14 @@ struct vc_volume {
     uint8_t* d_scratch = nullptr;
     size_t scratch_bytes = 0;
     uint64_t* d_counters = nullptr;
+    // per-stream scratch of the two-stage raycast: frame work counters and the
+    // first-hit queue (renders on different streams never share them)
+    struct StreamScratch {
+        void* work = nullptr;
+        void* hits = nullptr;
+        size_t hit_cap = 0;
+    };
+    std::unordered_map<cudaStream_t, StreamScratch> scratch;
     cudaStream_t host_stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::mutex mu;
@@ -135,6 +144,10 @@ void release(vc_volume* v) {
     for (auto& p : v->d_grad) cudaFree(p);
     cudaFree(v->d_scratch);
     cudaFree(v->d_counters);
+    for (auto& kv : v->scratch) {
+        cudaFree(kv.second.work);
+        cudaFree(kv.second.hits);
+    }
     if (v->host_stream) cudaStreamDestroy(v->host_stream);
     if (v->ev0) cudaEventDestroy(v->ev0);
     if (v->ev1) cudaEventDestroy(v->ev1);
@@ -232,6 +245,21 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
     L.out = d_rgba;
     L.local_rows = local_rows;
     L.counters = d_counters;
+    {
+        auto& sc = v->scratch[s];
+        const size_t need = (size_t)local_rows * p->width;
+        if (sc.work == nullptr) VC_CUDA(cudaMalloc(&sc.work, vc::frame_work_bytes()));
+        if (sc.hit_cap < need) {
+            cudaFree(sc.hits);
+            sc.hits = nullptr;
+            sc.hit_cap = 0;
+            cudaError_t e = cudaMalloc(&sc.hits, need * vc::hit_entry_bytes());
+            if (e != cudaSuccess) return fail(VC_ERR_NOMEM, std::string("cudaMalloc(hit queue): ") + cudaGetErrorString(e));
+            sc.hit_cap = need;
+        }
+        L.work = sc.work;
+        L.hits = sc.hits;
+    }
     L.mx = v->mx;
     L.my = v->my;
     L.occ = v->d_occ;

@@ -52,8 +52,8 @@ struct Ctx {
 
 // ceil(x) for 0 <= x < 2^31 without the XU pipe
 __device__ __forceinline__ double ceil_pos(double x) {
-    const double t = __dadd_rn(x, TWO52);
-    double r = __dsub_rn(t, TWO52);
+    const double t = __dadd_rn(x, MAGIC_RND);
+    double r = __dsub_rn(t, MAGIC_RND);
     if (r < x) r = __dadd_rn(r, 1.0);
     return r;
 }
@@ -84,29 +84,65 @@ __device__ __forceinline__ double skip_to(double t, double k, double base, const
     return kn;
 }
 
-// Is the lattice sample at position p skippable?  Returns true when it is
-// provably outside the window (no fetch needed) and updates k.
-template <typename T>
-__device__ __forceinline__ bool try_skip(const Ctx<T>& C, const double p[3], double t, double& k,
-                                         double base, unsigned& nskip) {
-    if (!in_range(C.v, p[0], p[1], p[2])) {  // reads 0, and 0 is outside the window
-        k += 1.0;
-        nskip += 1;
+__device__ __forceinline__ uint32_t macro_index(const Skip& sk, const Loc& L) {
+    return ((uint32_t)(L.k >> MC_SHIFT) * (uint32_t)sk.my + (uint32_t)(L.j >> MC_SHIFT)) * (uint32_t)sk.mx +
+           (uint32_t)(L.i >> MC_SHIFT);
+}
+
+// One lattice sample of the march: returns true and the value when it must
+// be evaluated (the reference's sample_any at p), false when empty-space
+// skipping proves it out of window, in which case k has been advanced.
+template <typename T, int INTERP>
+__device__ __forceinline__ bool march_sample(const Ctx<T>& C, const double p[3], double t, double& k,
+                                             double base, unsigned& nskip, double& val) {
+    if (INTERP != VC_TRILINEAR) {
+        if (C.sk.on && !in_range(C.v, p[0], p[1], p[2])) {  // reads 0, outside the window
+            k += 1.0;
+            nskip += 1;
+            return false;
+        }
+        if (C.sk.on) {
+            Loc L;
+            locate(C.v, p, L);
+            const int d = __ldg(C.sk.dist + macro_index(C.sk, L));
+            if (d != 0) {
+                const int c[3] = {L.i, L.j, L.k};
+                const double kn = skip_to(t, k, base, C.sk, p, c, d);
+                nskip += (unsigned)__double2uint_rz(kn - k);
+                k = kn;
+                return false;
+            }
+        }
+        val = sample_any<T, INTERP>(C.v, p[0], p[1], p[2]);
         return true;
     }
-    int c[3];
-    double f;
-    c[0] = cell(p[0], C.v.nx, C.v.cx, f);
-    c[1] = cell(p[1], C.v.ny, C.v.cy, f);
-    c[2] = cell(p[2], C.v.nz, C.v.cz, f);
-    const uint32_t m = ((uint32_t)(c[2] >> MC_SHIFT) * (uint32_t)C.sk.my + (uint32_t)(c[1] >> MC_SHIFT)) *
-                           (uint32_t)C.sk.mx + (uint32_t)(c[0] >> MC_SHIFT);
-    const int d = __ldg(C.sk.dist + m);
-    if (d == 0) return false;
-    const double kn = skip_to(t, k, base, C.sk, p, c, d);
-    nskip += (unsigned)__double2uint_rz(kn - k);
-    k = kn;
+    Loc L;
+    const bool inr = locate(C.v, p, L);
+    if (C.sk.on) {
+        if (!inr) {  // reads 0, and 0 is outside the window when skipping is on
+            k += 1.0;
+            nskip += 1;
+            return false;
+        }
+        const int d = __ldg(C.sk.dist + macro_index(C.sk, L));
+        if (d != 0) {
+            const int c[3] = {L.i, L.j, L.k};
+            const double kn = skip_to(t, k, base, C.sk, p, c, d);
+            nskip += (unsigned)__double2uint_rz(kn - k);
+            k = kn;
+            return false;
+        }
+    }
+    val = inr ? trilinear_at(C.v, L) : 0.0;
     return true;
+}
+
+// sample_any at p (fine scan, bisection)
+template <typename T, int INTERP>
+__device__ __forceinline__ double sample_at(const Ctx<T>& C, const double p[3]) {
+    if (INTERP != VC_TRILINEAR) return sample_any<T, INTERP>(C.v, p[0], p[1], p[2]);
+    Loc L;
+    return locate(C.v, p, L) ? trilinear_at(C.v, L) : 0.0;
 }
 
 // Trilinear interpolation of the packed gradient volume at an interior
@@ -206,21 +242,37 @@ __device__ __forceinline__ bool in_window(const vc_render_params& P, double v) {
     return P.t_low <= v && v <= P.t_high;
 }
 
-// One pixel as a single state machine, so the march loop and the shading
-// code each appear once in the binary:
-//   phase 0: march t_enter + k*coarse to the first in-window sample, fine
-//            backward scan, bisection (first_hit + bisect_window)
-//   phase 1: march t_star + m*coarse to the next in-window sample
-//            (composite loop, _kernels.py:755-790)
-// and one shading site.  Accumulation is arranged so the first shade's
-// acc = a*c, remain = 1 - a come out bit-identical to the reference
-// (1.0*a*c == a*c, 0.0 + x == x, 1.0*(1-a) == 1-a).
-template <typename T, int OP, int INTERP>
-__device__ __forceinline__ uchar4 trace_pixel(Ctx<T>& C, const vc_render_params& P, int px, int py,
-                                              unsigned& nsamp, unsigned& nshade, unsigned& nskip,
-                                              unsigned& nhit) {
-    const uchar4 bgq = make_uchar4(quant(P.bg[0]), quant(P.bg[1]), quant(P.bg[2]), quant(P.bg[3]));
-    // ray generation, _kernels.py:639-648
+// Per-lane ray state of the persistent kernel.  A pixel is traced as a
+// sequence of "events"; one event = march the lattice base + k*coarse to
+// the next in-window sample (+ fine backward scan and bisection for the
+// first one) and shade it.  The first event's lattice is t_enter + k*coarse
+// (first_hit, _kernels.py:401-465 + bisect_window :468-487); later events
+// march t_star + m*coarse (composite loop, :755-790).  Accumulation is
+// arranged so the first shade's acc = a*c, remain = 1 - a come out
+// bit-identical to the reference (1.0*a*c == a*c, 0.0 + x == x,
+// 1.0*(1-a) == 1-a).
+struct RayState {
+    double t_enter, lim, base, k;
+    double acc_r, acc_g, acc_b, remain;
+    double t_hit;    // lattice parameter of the in-window sample found by the march
+    bool found;      // march stopped on an in-window sample
+    bool exhausted;  // march ran past t_exit
+};
+
+__device__ __forceinline__ uchar4 bg_pixel(const vc_render_params& P) {
+    return make_uchar4(quant(P.bg[0]), quant(P.bg[1]), quant(P.bg[2]), quant(P.bg[3]));
+}
+
+// image row of local (packed) row lr under the band partition
+__device__ __forceinline__ int image_row(const vc_render_params& P, int lr) {
+    const int band = lr / P.band_rows, within = lr - band * P.band_rows;
+    return (P.band_first + band * P.band_step) * P.band_rows + within;
+}
+
+// ray generation (_kernels.py:639-648) + box interval (:649); false = miss
+template <typename T>
+__device__ __forceinline__ bool start_ray(Ctx<T>& C, const vc_render_params& P, int px, int py,
+                                          RayState& R) {
     const double v_ndc = dsub(1.0, ddiv(dmul(2.0, dadd((double)py, 0.5)), (double)P.height));
     const double u_ndc = dsub(ddiv(dmul(2.0, dadd((double)px, 0.5)), (double)P.width), 1.0);
     const double uw = dmul(u_ndc, P.half_w), vh = dmul(v_ndc, P.half_h);
@@ -231,154 +283,380 @@ __device__ __forceinline__ uchar4 trace_pixel(Ctx<T>& C, const vc_render_params&
 #pragma unroll
     for (int a = 0; a < 3; a++) {
         C.rp.d[a] = ddiv(d[a], dn);
-        C.rp.o[a] = P.eye[a];
         C.sk.ib[a] = C.rp.d[a] == 0.0 ? 0.0 : C.rp.s[a] / C.rp.d[a];
     }
-    C.sk.inv_coarse = 1.0 / P.coarse;
     double t_enter, t_exit;
-    if (!box_interval(C.rp.o, C.rp.d, P.clip_lo, P.clip_hi, t_enter, t_exit)) return bgq;
-    nhit++;
-    const double coarse = P.coarse, fine = P.fine;
-    const double lim = dadd(t_exit, 1e-12);
-
-    double base = t_enter, k = 0.0;  // lattice base and index (exact doubles)
-    bool composite = false;
-    double tcur = 0.0;
-    double acc_r = 0.0, acc_g = 0.0, acc_b = 0.0, remain = 1.0;
-    for (;;) {
-        // ---- march the lattice base + k*coarse to the next in-window sample
-        bool found = false;
-        double t = 0.0;
-        for (;;) {
-            t = dadd(base, dmul(k, coarse));
-            if (t > lim) break;
-            double p[3];
-            C.rp.at(t, p);
-            if (C.sk.on && try_skip(C, p, t, k, base, nskip)) continue;
-            nsamp++;
-            const double val = sample_any<T, INTERP>(C.v, p[0], p[1], p[2]);
-            k += 1.0;
-            if (in_window(P, val)) {
-                found = true;
-                break;
-            }
-        }
-        if (!found) {
-            if (!composite) return bgq;
-            break;
-        }
-        if (!composite) {
-            // fine backward scan (_kernels.py:419-436)
-            bool bracket = false;
-            double t_in = t, t_before = t;
-            const double floor_t = dsub(t_enter, 1e-12);
-            for (double j = 1.0;; j += 1.0) {
-                const double tb = dsub(t, dmul(j, fine));
-                if (tb < floor_t) {
-                    t_in = t_before = dsub(t, dmul(j - 1.0, fine));
-                    break;
-                }
-                double b[3];
-                C.rp.at(tb, b);
-                nsamp++;
-                const double vb = sample_any<T, INTERP>(C.v, b[0], b[1], b[2]);
-                if (!in_window(P, vb)) {
-                    t_in = dsub(t, dmul(j - 1.0, fine));
-                    t_before = tb;
-                    bracket = true;
-                    break;
-                }
-            }
-            // bisect_window (_kernels.py:468-487)
-            tcur = t_in;
-            if (bracket && P.refine_iters > 0) {
-                double tb = t_before, ta = t_in;
-                for (int it = 0; it < P.refine_iters; it++) {
-                    const double tm = dmul(0.5, dadd(tb, ta));
-                    double p[3];
-                    C.rp.at(tm, p);
-                    nsamp++;
-                    const double val = sample_any<T, INTERP>(C.v, p[0], p[1], p[2]);
-                    if (in_window(P, val)) ta = tm;
-                    else tb = tm;
-                }
-                tcur = ta;
-            }
-            base = tcur;
-            k = 1.0;
-        } else {
-            tcur = t;
-        }
-        // ---- shade (the one call site)
-        const Rgba s = shade_sample<T, OP, INTERP>(C, P, tcur);
-        nshade++;
-        if (P.mode == VC_SURFACE) return make_uchar4(quant(s.r), quant(s.g), quant(s.b), 255);
-        const double w = dmul(remain, s.a);
-        acc_r = dadd(acc_r, dmul(w, s.r));
-        acc_g = dadd(acc_g, dmul(w, s.g));
-        acc_b = dadd(acc_b, dmul(w, s.b));
-        remain = dmul(remain, dsub(1.0, s.a));
-        if (s.a >= OPAQUE_ALPHA || remain < MIN_REMAINING) break;
-        composite = true;
-    }
-    acc_r = dadd(acc_r, dmul(remain, P.bg[0]));
-    acc_g = dadd(acc_g, dmul(remain, P.bg[1]));
-    acc_b = dadd(acc_b, dmul(remain, P.bg[2]));
-    return make_uchar4(quant(acc_r), quant(acc_g), quant(acc_b), 255);
+    if (!box_interval(C.rp.o, C.rp.d, P.clip_lo, P.clip_hi, t_enter, t_exit)) return false;
+    R.t_enter = t_enter;
+    R.lim = dadd(t_exit, 1e-12);
+    R.base = t_enter;
+    R.k = 0.0;
+    R.acc_r = R.acc_g = R.acc_b = 0.0;
+    R.remain = 1.0;
+    R.t_hit = 0.0;
+    R.found = false;
+    R.exhausted = false;
+    return true;
 }
 
+// One lattice step of the march base + k*coarse (first_hit's loop body,
+// _kernels.py:410-436 / the composite loop :756-765).
+template <typename T, int INTERP>
+__device__ __forceinline__ void march_step(const Ctx<T>& C, const vc_render_params& P, RayState& R,
+                                           unsigned& nsamp, unsigned& nskip) {
+    const double t = dadd(R.base, dmul(R.k, P.coarse));
+    if (t > R.lim) {
+        R.exhausted = true;
+        return;
+    }
+    double p[3];
+    C.rp.at(t, p);
+    double val;
+    if (!march_sample<T, INTERP>(C, p, t, R.k, R.base, nskip, val)) return;
+    nsamp++;
+    R.k += 1.0;
+    if (in_window(P, val)) {
+        R.found = true;
+        R.t_hit = t;
+    }
+}
+
+// fine backward scan (_kernels.py:419-436) + bisect_window (:468-487) from
+// the first in-window lattice sample t; returns t_star
+template <typename T, int INTERP>
+__device__ __forceinline__ double refine_hit(const Ctx<T>& C, const vc_render_params& P, const RayState& R,
+                                             double t, unsigned& nsamp) {
+    const double fine = P.fine;
+    bool bracket = false;
+    double t_in = t, t_before = t;
+    const double floor_t = dsub(R.t_enter, 1e-12);
+    for (double j = 1.0;; j += 1.0) {
+        const double tb = dsub(t, dmul(j, fine));
+        if (tb < floor_t) {
+            t_in = t_before = dsub(t, dmul(j - 1.0, fine));
+            break;
+        }
+        double b[3];
+        C.rp.at(tb, b);
+        nsamp++;
+        const double vb = sample_at<T, INTERP>(C, b);
+        if (!in_window(P, vb)) {
+            t_in = dsub(t, dmul(j - 1.0, fine));
+            t_before = tb;
+            bracket = true;
+            break;
+        }
+    }
+    double tcur = t_in;
+    if (bracket && P.refine_iters > 0) {
+        double tb = t_before, ta = t_in;
+        for (int it = 0; it < P.refine_iters; it++) {
+            const double tm = dmul(0.5, dadd(tb, ta));
+            double p[3];
+            C.rp.at(tm, p);
+            nsamp++;
+            const double val = sample_at<T, INTERP>(C, p);
+            if (in_window(P, val)) ta = tm;
+            else tb = tm;
+        }
+        tcur = ta;
+    }
+    return tcur;
+}
+
+__device__ __forceinline__ uchar4 composite_pixel(const vc_render_params& P, const RayState& R) {
+    return make_uchar4(quant(dadd(R.acc_r, dmul(R.remain, P.bg[0]))),
+                       quant(dadd(R.acc_g, dmul(R.remain, P.bg[1]))),
+                       quant(dadd(R.acc_b, dmul(R.remain, P.bg[2]))), 255);
+}
+
+// Shade at tcur and composite front to back.  Accumulation is arranged so
+// the first shade's acc = a*c, remain = 1 - a come out bit-identical to the
+// reference (_kernels.py:744-754: 1.0*a*c == a*c, 0.0 + x == x,
+// 1.0*(1-a) == 1-a).  Returns true when the pixel is finished.
 template <typename T, int OP, int INTERP>
-__global__ void __launch_bounds__(128, 4) raycast_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
-                                                      const float4* __restrict__ grad, RayPos rp0,
-                                                      const uint8_t* __restrict__ occ, int mx, int my,
-                                                      int skip_on, uchar4* __restrict__ out,
-                                                      int local_rows, unsigned long long* counters) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int px = blockIdx.x * 16 + (warp & 1) * 8 + (lane & 7);
-    const int lr = blockIdx.y * 8 + (warp >> 1) * 4 + (lane >> 3);
+__device__ __forceinline__ bool shade_and_composite(const Ctx<T>& C, const vc_render_params& P, RayState& R,
+                                                    double tcur, uchar4& out, unsigned& nshade) {
+    const Rgba s = shade_sample<T, OP, INTERP>(C, P, tcur);
+    nshade++;
+    if (P.mode == VC_SURFACE) {
+        out = make_uchar4(quant(s.r), quant(s.g), quant(s.b), 255);
+        return true;
+    }
+    const double w = dmul(R.remain, s.a);
+    R.acc_r = dadd(R.acc_r, dmul(w, s.r));
+    R.acc_g = dadd(R.acc_g, dmul(w, s.g));
+    R.acc_b = dadd(R.acc_b, dmul(w, s.b));
+    R.remain = dmul(R.remain, dsub(1.0, s.a));
+    if (s.a >= OPAQUE_ALPHA || R.remain < MIN_REMAINING) {
+        out = composite_pixel(P, R);
+        return true;
+    }
+    return false;
+}
+
+// a warp leaves the march loop when READY_NUM / READY_DEN of its live lanes
+// have a hit (or an exhausted ray) to resolve
+#ifndef VC_READY_NUM
+#define VC_READY_NUM 4
+#endif
+constexpr int READY_NUM = VC_READY_NUM, READY_DEN = 4;
+
+struct HitEntry {  // first-hit queue: pixel + refined parameter t_star
+    double t_star;
+    int lr, px;
+};
+
+// Work counters of one launch pair (zeroed together before the frame).
+struct FrameWork {
+    unsigned pixels;  // kernel A: next pixel work item
+    unsigned hits;    // kernel A -> B: queue length
+    unsigned shades;  // kernel B: next queue entry
+    unsigned pad;
+};
+
+template <typename T>
+__device__ __forceinline__ void init_ctx(Ctx<T>& C, const vc_render_params& P, const Vol<T>& vol,
+                                         const float4* grad, const RayPos& rp0, const uint8_t* dist, int mx,
+                                         int my, int skip_on) {
+    C.v = vol;
+    C.grad = grad;
+    C.rp = rp0;
+#pragma unroll
+    for (int a = 0; a < 3; a++) C.rp.o[a] = P.eye[a];
+    C.sk.dist = dist;
+    C.sk.mx = mx;
+    C.sk.my = my;
+    C.sk.on = skip_on != 0;
+    C.sk.inv_coarse = 1.0 / P.coarse;
+}
+
+__device__ __forceinline__ void commit_counters(unsigned long long* counters, unsigned nsamp, unsigned nshade,
+                                                unsigned nskip, unsigned nhit) {
+    if (counters == nullptr) return;
+    const unsigned FULL = 0xffffffffu;
+    nsamp = __reduce_add_sync(FULL, nsamp);
+    nshade = __reduce_add_sync(FULL, nshade);
+    nskip = __reduce_add_sync(FULL, nskip);
+    nhit = __reduce_add_sync(FULL, nhit);
+    if ((threadIdx.x & 31) == 0) {
+        if (nsamp) atomicAdd(counters + 0, (unsigned long long)nsamp);
+        if (nshade) atomicAdd(counters + 1, (unsigned long long)nshade);
+        if (nskip) atomicAdd(counters + 2, (unsigned long long)nskip);
+        if (nhit) atomicAdd(counters + 3, (unsigned long long)nhit);
+    }
+}
+
+// Warp-aggregated ticket: every lane with `want` gets a distinct index from
+// *ctr (one atomic per warp).
+__device__ __forceinline__ unsigned warp_ticket(unsigned* ctr, bool want) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned m = __ballot_sync(FULL, want);
+    unsigned base = 0;
+    const int leader = __ffs(m) - 1;
+    if (m != 0 && lane == leader) base = atomicAdd(ctr, (unsigned)__popc(m));
+    base = __shfl_sync(FULL, base, leader < 0 ? 0 : leader);
+    return base + __popc(m & ((1u << lane) - 1u));
+}
+
+// Kernel A -- first hit (wavefront stage 1).  Persistent CTAs; each lane
+// pulls pixels from FrameWork::pixels.  Work item w is lane (w % 32) of the
+// 8x4 screen tile w / 32 (tiles row-major), so a warp refilled as a whole
+// traces a compact tile (L1 locality).  The march runs in lock-step, one
+// lattice sample per trip, until every live lane has stopped (hit or ray
+// end); then hits are refined (fine scan + bisection) and pushed to the hit
+// queue, misses write the background, and finished lanes take new pixels:
+// the dynamic ray refill of Aila & Laine keeps warps full although
+// neighbouring rays march for very different lengths.
+template <typename T, int OP, int INTERP>
+__global__ void __launch_bounds__(128, 4) firsthit_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
+                                                          RayPos rp0, const uint8_t* __restrict__ dist, int mx,
+                                                          int my, int skip_on, uchar4* __restrict__ out,
+                                                          int local_rows, unsigned long long* counters,
+                                                          FrameWork* work, HitEntry* __restrict__ hits) {
+    const unsigned FULL = 0xffffffffu;
+    const int tiles_x = (P.width + 7) >> 3;
+    const unsigned total = (unsigned)tiles_x * (unsigned)((local_rows + 3) >> 2) * 32u;
+    Ctx<T> C;
+    init_ctx(C, P, vol, nullptr, rp0, dist, mx, my, skip_on);
     unsigned nsamp = 0, nshade = 0, nskip = 0, nhit = 0;
-    if (px < P.width && lr < local_rows) {
-        const int band = lr / P.band_rows, within = lr - band * P.band_rows;
-        const int py = (P.band_first + band * P.band_step) * P.band_rows + within;
-        if (py < P.height) {
-            Ctx<T> C;
-            C.v = vol;
-            C.grad = grad;
-            C.rp = rp0;
-            C.sk.dist = occ;
-            C.sk.mx = mx;
-            C.sk.my = my;
-            C.sk.on = skip_on != 0;
-            out[(size_t)lr * P.width + px] =
-                trace_pixel<T, OP, INTERP>(C, P, px, py, nsamp, nshade, nskip, nhit);
+    RayState R;
+    int px = 0, lr = 0;
+    bool active = false, done = false;
+    for (;;) {
+        for (;;) {  // refill idle lanes until each has a live ray or the frame is exhausted
+            const bool want = !active && !done;
+            if (__ballot_sync(FULL, want) == 0) break;
+            const unsigned w = warp_ticket(&work->pixels, want);
+            if (want) {
+                if (w >= total) {
+                    done = true;
+                } else {
+                    const unsigned tile = w >> 5, r = w & 31u;
+                    px = (int)(tile % (unsigned)tiles_x) * 8 + (int)(r & 7u);
+                    lr = (int)(tile / (unsigned)tiles_x) * 4 + (int)(r >> 3);
+                    if (px < P.width && lr < local_rows) {
+                        if (start_ray(C, P, px, image_row(P, lr), R)) {
+                            active = true;
+                            nhit++;
+                        } else {
+                            out[(size_t)lr * P.width + px] = bg_pixel(P);
+                        }
+                    }
+                }
+            }
+        }
+        if (__all_sync(FULL, done)) break;
+        for (;;) {
+            const bool need = active && !R.found && !R.exhausted;
+            const unsigned mneed = __ballot_sync(FULL, need);
+            if (mneed == 0) break;
+            const unsigned mact = __ballot_sync(FULL, active);
+            if (__popc(mact & ~mneed) * READY_DEN >= __popc(mact) * READY_NUM) break;
+            if (need) march_step<T, INTERP>(C, P, R, nsamp, nskip);
+        }
+        const bool hit = active && R.found;
+        double t_star = 0.0;
+        if (hit) t_star = refine_hit<T, INTERP>(C, P, R, R.t_hit, nsamp);
+        const unsigned q = warp_ticket(&work->hits, hit);
+        if (hit) {
+            HitEntry e;
+            e.t_star = t_star;
+            e.lr = lr;
+            e.px = px;
+            hits[q] = e;
+        }
+        if (active && (R.found || R.exhausted)) {
+            if (R.exhausted) out[(size_t)lr * P.width + px] = bg_pixel(P);
+            active = false;
         }
     }
-    if (counters != nullptr) {
-        nsamp = __reduce_add_sync(0xffffffffu, nsamp);
-        nshade = __reduce_add_sync(0xffffffffu, nshade);
-        nskip = __reduce_add_sync(0xffffffffu, nskip);
-        nhit = __reduce_add_sync(0xffffffffu, nhit);
-        if (lane == 0) {
-            if (nsamp) atomicAdd(counters + 0, (unsigned long long)nsamp);
-            if (nshade) atomicAdd(counters + 1, (unsigned long long)nshade);
-            if (nskip) atomicAdd(counters + 2, (unsigned long long)nskip);
-            if (nhit) atomicAdd(counters + 3, (unsigned long long)nhit);
+    commit_counters(counters, nsamp, nshade, nskip, nhit);
+}
+
+// Kernel B -- shade + composite (wavefront stage 2).  Persistent CTAs pull
+// first hits from the queue, regenerate the ray, shade at t_star and, in
+// composited mode, keep marching t_star + m*coarse and shading in-window
+// samples until early ray termination or the ray leaves the box.  Lanes
+// refill from the queue as their pixel finishes.
+template <typename T, int OP, int INTERP>
+__global__ void __launch_bounds__(128, 4) shade_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
+                                                       const float4* __restrict__ grad, RayPos rp0,
+                                                       const uint8_t* __restrict__ dist, int mx, int my,
+                                                       int skip_on, uchar4* __restrict__ out,
+                                                       unsigned long long* counters, FrameWork* work,
+                                                       const HitEntry* __restrict__ hits) {
+    const unsigned FULL = 0xffffffffu;
+    const unsigned total = *(volatile unsigned*)&work->hits;
+    Ctx<T> C;
+    init_ctx(C, P, vol, grad, rp0, dist, mx, my, skip_on);
+    unsigned nsamp = 0, nshade = 0, nskip = 0, nhit = 0;
+    RayState R;
+    int px = 0, lr = 0;
+    bool active = false, done = false;
+    for (;;) {
+        for (;;) {
+            const bool want = !active && !done;
+            if (__ballot_sync(FULL, want) == 0) break;
+            const unsigned q = warp_ticket(&work->shades, want);
+            bool fresh = false;
+            double t_star = 0.0;
+            if (want) {
+                if (q >= total) {
+                    done = true;
+                } else {
+                    const HitEntry e = hits[q];
+                    px = e.px;
+                    lr = e.lr;
+                    t_star = e.t_star;
+                    start_ray(C, P, px, image_row(P, lr), R);  // a queued ray hit the box
+                    R.base = t_star;
+                    R.k = 1.0;
+                    fresh = true;
+                }
+            }
+            // the first shade of every fresh ray, all lanes together
+            if (__ballot_sync(FULL, fresh) != 0 && fresh) {
+                uchar4 o;
+                if (shade_and_composite<T, OP, INTERP>(C, P, R, t_star, o, nshade)) {
+                    out[(size_t)lr * P.width + px] = o;
+                } else {
+                    active = true;
+                }
+            }
+        }
+        if (__all_sync(FULL, done)) break;
+        for (;;) {
+            const bool need = active && !R.found && !R.exhausted;
+            const unsigned mneed = __ballot_sync(FULL, need);
+            if (mneed == 0) break;
+            const unsigned mact = __ballot_sync(FULL, active);
+            if (__popc(mact & ~mneed) * READY_DEN >= __popc(mact) * READY_NUM) break;
+            if (need) march_step<T, INTERP>(C, P, R, nsamp, nskip);
+        }
+        if (active && (R.found || R.exhausted)) {
+            uchar4 o;
+            bool fin;
+            if (R.exhausted) {
+                o = composite_pixel(P, R);
+                fin = true;
+            } else {
+                R.found = false;
+                fin = shade_and_composite<T, OP, INTERP>(C, P, R, R.t_hit, o, nshade);
+            }
+            if (fin) {
+                out[(size_t)lr * P.width + px] = o;
+                active = false;
+            }
         }
     }
+    commit_counters(counters, nsamp, nshade, nskip, nhit);
 }
 
 }  // namespace vc
 
 namespace vc {
 
+static int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <typename K>
+static unsigned persistent_blocks(K kernel, long long max_useful) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, 0);
+    if (per_sm < 1) per_sm = 1;
+    long long b = (long long)sm_count() * per_sm;
+    if (b > max_useful) b = max_useful;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
 template <typename T, int OP, int INTERP>
 static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
     const Vol<T> vol = make_vol(static_cast<const T*>(L.data), L.nx, L.ny, L.nz);
-    const dim3 block(128);
-    const dim3 grid((L.p->width + 15) / 16, (L.local_rows + 7) / 8);
-    raycast_kernel<T, OP, INTERP><<<grid, block, 0, stream>>>(
-        *L.p, vol, static_cast<const float4*>(L.grad), L.rp, L.occ, L.mx, L.my, L.skip_on,
-        reinterpret_cast<uchar4*>(L.out), L.local_rows, reinterpret_cast<unsigned long long*>(L.counters));
+    FrameWork* fw = reinterpret_cast<FrameWork*>(L.work);
+    HitEntry* hits = reinterpret_cast<HitEntry*>(L.hits);
+    cudaError_t e = cudaMemsetAsync(fw, 0, sizeof(FrameWork), stream);
+    if (e != cudaSuccess) return e;
+    const long long tiles = (long long)((L.p->width + 7) / 8) * ((L.local_rows + 3) / 4);
+    firsthit_kernel<T, OP, INTERP><<<persistent_blocks(firsthit_kernel<T, OP, INTERP>, (tiles + 3) / 4), 128, 0,
+                                     stream>>>(*L.p, vol, L.rp, L.occ, L.mx, L.my, L.skip_on,
+                                               reinterpret_cast<uchar4*>(L.out), L.local_rows,
+                                               reinterpret_cast<unsigned long long*>(L.counters), fw, hits);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    shade_kernel<T, OP, INTERP><<<persistent_blocks(shade_kernel<T, OP, INTERP>, (tiles + 3) / 4), 128, 0,
+                                  stream>>>(*L.p, vol, static_cast<const float4*>(L.grad), L.rp, L.occ, L.mx,
+                                            L.my, L.skip_on, reinterpret_cast<uchar4*>(L.out),
+                                            reinterpret_cast<unsigned long long*>(L.counters), fw, hits);
     return cudaGetLastError();
 }
 
@@ -407,5 +685,8 @@ cudaError_t launch_raycast(const RenderLaunch& L, cudaStream_t s) {
         default: return launch_dtype<float>(L, s);
     }
 }
+
+size_t hit_entry_bytes() { return sizeof(HitEntry); }
+size_t frame_work_bytes() { return sizeof(FrameWork); }
 
 }  // namespace vc

@@ -93,11 +93,14 @@ __device__ __forceinline__ double biased2d(uint32_t biased) {
     return __dsub_rn(__hiloint2double(0x43300000, (int)biased), TWO52_31);
 }
 
-// floor(x) for 0 <= x < 2^31: returns the integer, r = (double)floor(x)
+// floor(x) for |x| < 2^31: returns the integer, r = (double)floor(x).
+// x + 1.5*2^52 lies in [2^52, 2^53) where the ulp is 1, so the sum is x
+// rounded to the nearest integer and its low word is that integer.
+constexpr double MAGIC_RND = 0x1.8p52;
 __device__ __forceinline__ int floor_pos(double x, double& r) {
-    const double t = __dadd_rn(x, TWO52);  // round-to-nearest-even integer
+    const double t = __dadd_rn(x, MAGIC_RND);
     int i = __double2loint(t);
-    r = __dsub_rn(t, TWO52);
+    r = __dsub_rn(t, MAGIC_RND);
     if (r > x) {
         r = __dsub_rn(r, 1.0);
         i -= 1;
@@ -174,6 +177,55 @@ __device__ __forceinline__ double sample_trilinear(const Vol<T>& v, double x, do
     const double y0 = lerp(x00, x10, fy);
     const double y1 = lerp(x01, x11, fy);
     return lerp(y0, y1, fz);
+}
+
+// Cell location of a position, computed once and shared by the range
+// check, the macrocell lookup and the trilinear gather.  Valid for
+// |coordinate| < 2^31 (ray positions stay within the volume box).
+struct Loc {
+    int i, j, k;        // lower cell corner, clamped like _kernels.py:52-64
+    double fx, fy, fz;  // fractions v - i0
+};
+
+__device__ __forceinline__ bool locate_axis(double x, int n, double nm1, double nm2, int& i0, double& f) {
+    double r;
+    int i = floor_pos(x, r);  // exact floor for negative x too
+    // in range  <=>  0 <= x <= n-1  <=>  i >= 0 and (i <= n-2 or x == n-1)
+    const bool inr = i >= 0 && (i <= n - 2 || x == nm1);
+    if (i > n - 2) {
+        i = n - 2 < 0 ? 0 : n - 2;
+        r = nm2;
+    }
+    i0 = i;
+    f = dsub(x, r);
+    return inr;
+}
+
+template <typename T>
+__device__ __forceinline__ bool locate(const Vol<T>& v, const double p[3], Loc& L) {
+    const bool a = locate_axis(p[0], v.nx, v.mx, v.cx, L.i, L.fx);
+    const bool b = locate_axis(p[1], v.ny, v.my, v.cy, L.j, L.fy);
+    const bool c = locate_axis(p[2], v.nz, v.mz, v.cz, L.k, L.fz);
+    return a && b && c;
+}
+
+// sample_trilinear (_kernels.py:104-115) from a precomputed in-range Loc
+template <typename T>
+__device__ __forceinline__ double trilinear_at(const Vol<T>& v, const Loc& L) {
+    const uint32_t sx = L.i + 1 < v.nx ? 1u : 0u;
+    const uint32_t sy = L.j + 1 < v.ny ? (uint32_t)v.nx : 0u;
+    const uint32_t sz = L.k + 1 < v.nz ? (uint32_t)v.nx * (uint32_t)v.ny : 0u;
+    const T* b = v.data + (((uint32_t)L.k * (uint32_t)v.ny + (uint32_t)L.j) * (uint32_t)v.nx + (uint32_t)L.i);
+    const T c000 = ldv(b), c100 = ldv(b + sx), c010 = ldv(b + sy), c110 = ldv(b + sy + sx);
+    const T c001 = ldv(b + sz), c101 = ldv(b + sz + sx), c011 = ldv(b + sz + sy),
+            c111 = ldv(b + sz + sy + sx);
+    const double x00 = lerp_vox<T>(c000, c100, L.fx);
+    const double x10 = lerp_vox<T>(c010, c110, L.fx);
+    const double x01 = lerp_vox<T>(c001, c101, L.fx);
+    const double x11 = lerp_vox<T>(c011, c111, L.fx);
+    const double y0 = lerp(x00, x10, L.fy);
+    const double y1 = lerp(x01, x11, L.fy);
+    return lerp(y0, y1, L.fz);
 }
 
 // _kernels.py:67-72

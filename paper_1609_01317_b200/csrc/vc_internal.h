@@ -22,9 +22,13 @@ struct RenderLaunch {
     uint8_t* out;         // local_rows x width x 4
     int local_rows;
     uint64_t* counters;   // VC_NUM_COUNTERS or nullptr
+    void* work;           // frame work counters (FrameWork, zeroed per launch)
+    void* hits;           // first-hit queue, >= local_rows * width entries
 };
 
 cudaError_t launch_raycast(const RenderLaunch& L, cudaStream_t s);
+size_t hit_entry_bytes();
+size_t frame_work_bytes();
 
 // Kernel 1 (gradient_prepass.cu)
 cudaError_t launch_gradient_prepass(int dtype, const void* data, int nx, int ny, int nz, int op,
