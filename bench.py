@@ -44,8 +44,8 @@ UNIT = "frames/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--size", type=int, default=512)
     ap.add_argument("--width", type=int, default=1920)
@@ -81,29 +81,43 @@ def lscpu_model() -> str:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
-
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clocks and throttle reasons sampled (NVML, every 20 ms) during the
+    timed region; falls back to nvidia-smi when NVML is unavailable."""
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            n = self._nvml
+            sm = n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM)
+            mx = n.nvmlDeviceGetMaxClockInfo(self._h, n.NVML_CLOCK_SM)
+            rs = n.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            return float(sm), float(mx), int(rs)
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip().split(",")
+        return float(out[0]), float(out[1]), 0
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self.samples.append(self._sample())
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.02)
 
     def __enter__(self):
         self._t.start()
@@ -115,15 +129,13 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        names = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                 0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+        reasons = sorted({nm for _, _, r in self.samples for bit, nm in names.items() if r & bit})
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def peaks():
@@ -305,36 +317,44 @@ def run_ours(args):
     fps = args.steps / (ms_total / 1000.0)
 
     # brute-force work counts of the timed frames (our skip-off counts equal
-    # the reference's sample counts, tests/test_gpu_parity.py), untimed
-    cnt = torch.zeros(4, dtype=torch.int64, device=f"cuda:{dev}")
-    Wt = Kt = 0
+    # the reference's sample counts, tests/test_gpu_parity.py), untimed; per
+    # stage: counters [4] / [5] split the samples between the two kernels
+    from dataclasses import replace
+
+    cnt = torch.zeros(_native.NUM_COUNTERS, dtype=torch.int64, device=f"cuda:{dev}")
+    tot = np.zeros(_native.NUM_COUNTERS, np.float64)
     nsub = min(args.steps, 6)
     for k in range(nsub):
         sc, st = frame(args.warmup + k)
-        from dataclasses import replace
-
         P = render_params(vol, sc, replace(st, use_octree=False, gradient_source="taps"),
                           band_rows=plan.band_rows, band_first=rank, band_step=world)
         _native.check(L.vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(local_buf.data_ptr()),
                                   ctypes.c_void_p(cnt.data_ptr()), sp))
         torch.cuda.synchronize(dev)
-        c = cnt.cpu().numpy()
-        Wt += int(c[0]) + int(c[1])
-        Kt += int(c[1])
+        tot += cnt.cpu().numpy()
     if world > 1:
-        t = torch.tensor([Wt, Kt], dtype=torch.int64, device=f"cuda:{dev}")
+        t = torch.tensor(tot, dtype=torch.float64, device=f"cuda:{dev}")
         torch.distributed.all_reduce(t)
-        Wt, Kt = (int(x) for x in t.cpu().numpy())
-    w_frame = Wt / nsub
-    k_frame = Kt / nsub
+        tot = t.cpu().numpy()
+    bf = tot / nsub  # brute force per frame
+    w_frame = bf[0] + bf[1]  # ray samples incl. each shade's value sample
+    k_frame = bf[1]
 
-    # executed work of the timed configuration (skipping on)
-    sc, st = frame(args.warmup)
-    P = render_params(vol, sc, st, band_rows=plan.band_rows, band_first=rank, band_step=world)
-    _native.check(L.vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(local_buf.data_ptr()),
-                              ctypes.c_void_p(cnt.data_ptr()), sp))
-    torch.cuda.synchronize(dev)
-    ce = cnt.cpu().numpy().tolist()
+    # executed work and per-stage device time of the timed configuration
+    stage = np.zeros(2)
+    ce = np.zeros(_native.NUM_COUNTERS)
+    nprof = min(args.steps, 20)
+    sms = (ctypes.c_float * 2)()
+    for k in range(nprof):
+        sc, st = frame(args.warmup + k)
+        P = render_params(vol, sc, st, band_rows=plan.band_rows, band_first=rank, band_step=world)
+        flush.zero_()
+        _native.check(L.vc_render_profiled(dv.handle, ctypes.byref(P), ctypes.c_void_p(local_buf.data_ptr()),
+                                           ctypes.c_void_p(cnt.data_ptr()), sp, sms))
+        stage += np.array([sms[0], sms[1]])
+        ce += cnt.cpu().numpy()
+    stage /= nprof
+    ce /= nprof
 
     # parity spot check of the timed configuration vs the bit-faithful taps path
     parity = None
@@ -380,10 +400,15 @@ def run_ours(args):
                          f"cpu: {lscpu_model()}"}
 
     bpv = vol.data.dtype.itemsize
-    alg_bytes = 8 * bpv * w_frame + 128 * k_frame + 4 * H * W
-    avg_ms = float(np.mean(step_ms))
-    achieved = alg_bytes / (avg_ms / 1000.0) / 1e9
+    # algorithmic (logical) bytes: 8*bpv per ray sample,
+    # 128 per shade (8 float4 gradient taps), 4 per output pixel
+    alg_frame = 8 * bpv * w_frame + 128 * k_frame + 4 * H * W
+    alg_stage = [8 * bpv * bf[4], 8 * bpv * (bf[5] + k_frame) + 128 * k_frame + 4 * H * W]
+    dom = int(np.argmax(stage))
+    names = ["vc::firsthit_kernel", "vc::shade_kernel"]
     peak, peak_kind = peaks()
+    achieved = alg_stage[dom] / (stage[dom] / 1000.0) / 1e9
+    frame_ms = float(np.mean(step_ms))
     traffic = profiled_traffic()
     line = {
         "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -398,17 +423,25 @@ def run_ours(args):
                    "parallelism": f"image-plane row bands x{world}"},
         "gsamples_per_s": w_frame * fps / 1e9,
         "work_per_frame": {"W_ray_samples_bruteforce": w_frame, "K_shades": k_frame,
-                           "executed": {"samples": ce[0], "shades": ce[1], "skipped": ce[2],
-                                        "rays_in_box": ce[3]}},
+                           "executed": {"samples": float(ce[0]), "shades": float(ce[1]),
+                                        "skipped": float(ce[2]), "rays_in_box": float(ce[3])}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": (traffic or {}).get("bytes_per_launch"),
-                     "kernel": "vc::raycast_kernel", "peak_source": peak_kind,
-                     "algorithmic_bytes_per_launch": alg_bytes,
-                     "note": "logical bytes 8*bpv*W + 128*K + 4*pixels (SURVEY.md 8(d)); the kernel "
-                             "is gather/FP64 bound, HBM is the stated denominator"},
+                     "frac": achieved / peak,
+                     "traffic": (traffic or {}).get(names[dom], {}).get("dram_bytes_per_launch"),
+                     "kernel": names[dom], "peak_source": peak_kind,
+                     "launch_ms": float(stage[dom]), "algorithmic_bytes_per_launch": alg_stage[dom],
+                     "stages_ms": {names[0]: float(stage[0]), names[1]: float(stage[1])},
+                     "frame": {"achieved": alg_frame / (frame_ms / 1000.0) / 1e9,
+                               "frac": alg_frame / (frame_ms / 1000.0) / 1e9 / peak,
+                               "algorithmic_bytes": alg_frame},
+                     "note": "logical bytes 8*bpv per ray sample + 128 per shade + 4 per pixel "
+                             "(SURVEY.md 8(d)), brute-force counts; the kernels are L1-gather/FP64 "
+                             "bound, HBM is the stated denominator"},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": args.steps,
+        "gpu_launches": 2 * args.steps,
+        "gpu_launches_note": "per frame: vc::firsthit_kernel + vc::shade_kernel (+ one cudaMemsetAsync "
+                             "of the work counters)",
         "clocks": clk.summary(),
         "parity": parity,
         "wall_s_timed_region": t_wall,

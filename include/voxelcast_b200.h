@@ -104,15 +104,17 @@ typedef struct vc_render_params {
     int32_t grad_source;                /* vc_grad_source */
 } vc_render_params;
 
-/* counters written by vc_render (device, 4 x uint64):
+/* counters written by vc_render (device, VC_NUM_COUNTERS x uint64):
  *   [0] volume samples taken by marching, fine scan, bisection and the
  *       composite loop (each one sample_any call in the reference)
  *   [1] shades (each _shade_sample call: 1 value sample + GRAD_SAMPLES taps)
  *   [2] lattice samples skipped by empty-space skipping
  *   [3] pixels whose ray hit the volume box
+ *   [4] of [0], samples taken by the first-hit stage (march, fine scan, bisection)
+ *   [5] of [0], samples taken by the shade stage (composite march)
  * The reference's FrameBuffer.sample_count (raycast.py:513) equals
  * c[0] + c[1] * (1 + GRAD_SAMPLES[op]) when skip_empty == 0. */
-#define VC_NUM_COUNTERS 4
+#define VC_NUM_COUNTERS 6
 
 VC_API int vc_abi_version(void);
 /* sizeof(vc_render_params), so bindings can check their struct mirror */
@@ -147,6 +149,11 @@ VC_API int vc_gradient_prepass_into(const vc_volume *vol, int op, void *d_out, v
  * d_counters may be NULL. */
 VC_API int vc_render(vc_volume *vol, const vc_render_params *p, uint8_t *d_rgba, uint64_t *d_counters,
               void *stream);
+/* vc_render plus per-stage device time (synchronous): stage_ms[0] = the
+ * first-hit stage (ray generation, march, fine scan, bisection), stage_ms[1]
+ * = the shade / composite stage.  For profiling and the roofline report. */
+VC_API int vc_render_profiled(vc_volume *vol, const vc_render_params *p, uint8_t *d_rgba,
+                              uint64_t *d_counters, void *stream, float *stage_ms);
 /* render_frame end to end: render, copy the frame to host memory h_rgba
  * (pinned or pageable), counters to h_counters (may be NULL); synchronous.
  * *ms (may be NULL) = device time of render + copy (CUDA events). */

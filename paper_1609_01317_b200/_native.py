@@ -26,7 +26,7 @@ VC_ERR_UNSUPPORTED = 4
 VC_U8, VC_U16, VC_F32 = 0, 1, 2
 VC_GRAD_TAPS, VC_GRAD_VOLUME = 0, 1
 MAX_LUT = 64
-NUM_COUNTERS = 4
+NUM_COUNTERS = 6
 
 DTYPE_CODES = {np.dtype(np.uint8): VC_U8, np.dtype(np.uint16): VC_U16, np.dtype(np.float32): VC_F32}
 
@@ -35,7 +35,7 @@ EXPORTS = (
     "vc_abi_version", "vc_render_params_size", "vc_last_error", "vc_device_count",
     "vc_volume_create", "vc_volume_create_device", "vc_volume_destroy", "vc_volume_data",
     "vc_gradient_prepass", "vc_gradient_volume", "vc_gradient_prepass_into",
-    "vc_render", "vc_render_host",
+    "vc_render", "vc_render_profiled", "vc_render_host",
     "vc_sample_points", "vc_gradient_points",
     "vc_box_interval_rays", "vc_first_hit_rays", "vc_bisect_rays",
 )
@@ -108,6 +108,8 @@ def load(build_if_missing: bool = True):
             "vc_gradient_volume": ([vp, ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
             "vc_gradient_prepass_into": ([vp, ctypes.c_int, vp, vp], ctypes.c_int),
             "vc_render": ([vp, ctypes.POINTER(RenderParams), vp, vp, vp], ctypes.c_int),
+            "vc_render_profiled": ([vp, ctypes.POINTER(RenderParams), vp, vp, vp,
+                                    ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
             "vc_render_host": ([vp, ctypes.POINTER(RenderParams), vp, u64p,
                                 ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
             "vc_sample_points": ([vp, ctypes.c_int, dp, i64, dp], ctypes.c_int),

@@ -233,8 +233,10 @@ int validate_params(const vc_render_params* p, int* local_rows) {
 }
 
 int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64_t* d_counters,
-                cudaStream_t s, int local_rows) {
+                cudaStream_t s, int local_rows, cudaEvent_t* stage_events = nullptr) {
     vc::RenderLaunch L{};
+    if (stage_events)
+        for (int i = 0; i < 3; i++) L.ev[i] = stage_events[i];
     L.p = p;
     L.dtype = v->dtype;
     L.data = v->d_data;
@@ -356,6 +358,29 @@ int vc_render(vc_volume* vol, const vc_render_params* p, uint8_t* d_rgba, uint64
     DeviceGuard g(vol->device);
     std::lock_guard<std::mutex> lk(vol->mu);
     return render_impl(vol, p, d_rgba, d_counters, static_cast<cudaStream_t>(stream), local_rows);
+}
+
+int vc_render_profiled(vc_volume* vol, const vc_render_params* p, uint8_t* d_rgba, uint64_t* d_counters,
+                       void* stream, float* stage_ms) {
+    if (!vol || !stage_ms) return fail(VC_ERR_INVALID, "null argument");
+    int local_rows = 0;
+    int rc = validate_params(p, &local_rows);
+    if (rc) return rc;
+    if (!d_rgba && local_rows > 0) return fail(VC_ERR_INVALID, "output buffer is null");
+    DeviceGuard g(vol->device);
+    std::lock_guard<std::mutex> lk(vol->mu);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    for (auto& e : ev) VC_CUDA(cudaEventCreate(&e));
+    rc = render_impl(vol, p, d_rgba, d_counters, s, local_rows, ev);
+    if (rc == VC_OK) {
+        cudaError_t e = cudaEventSynchronize(ev[2]);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&stage_ms[0], ev[0], ev[1]);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&stage_ms[1], ev[1], ev[2]);
+        if (e != cudaSuccess) rc = cuda_fail(e, "stage timing");
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    return rc;
 }
 
 int vc_render_host(vc_volume* vol, const vc_render_params* p, uint8_t* h_rgba, uint64_t* h_counters,

@@ -431,8 +431,8 @@ __device__ __forceinline__ void init_ctx(Ctx<T>& C, const vc_render_params& P, c
     C.sk.inv_coarse = 1.0 / P.coarse;
 }
 
-__device__ __forceinline__ void commit_counters(unsigned long long* counters, unsigned nsamp, unsigned nshade,
-                                                unsigned nskip, unsigned nhit) {
+__device__ __forceinline__ void commit_counters(unsigned long long* counters, int stage, unsigned nsamp,
+                                                unsigned nshade, unsigned nskip, unsigned nhit) {
     if (counters == nullptr) return;
     const unsigned FULL = 0xffffffffu;
     nsamp = __reduce_add_sync(FULL, nsamp);
@@ -441,6 +441,7 @@ __device__ __forceinline__ void commit_counters(unsigned long long* counters, un
     nhit = __reduce_add_sync(FULL, nhit);
     if ((threadIdx.x & 31) == 0) {
         if (nsamp) atomicAdd(counters + 0, (unsigned long long)nsamp);
+        if (nsamp) atomicAdd(counters + 4 + stage, (unsigned long long)nsamp);
         if (nshade) atomicAdd(counters + 1, (unsigned long long)nshade);
         if (nskip) atomicAdd(counters + 2, (unsigned long long)nskip);
         if (nhit) atomicAdd(counters + 3, (unsigned long long)nhit);
@@ -532,7 +533,7 @@ __global__ void __launch_bounds__(128, 4) firsthit_kernel(const __grid_constant_
             active = false;
         }
     }
-    commit_counters(counters, nsamp, nshade, nskip, nhit);
+    commit_counters(counters, 0, nsamp, nshade, nskip, nhit);
 }
 
 // Kernel B -- shade + composite (wavefront stage 2).  Persistent CTAs pull
@@ -611,7 +612,7 @@ __global__ void __launch_bounds__(128, 4) shade_kernel(const __grid_constant__ v
             }
         }
     }
-    commit_counters(counters, nsamp, nshade, nskip, nhit);
+    commit_counters(counters, 1, nsamp, nshade, nskip, nhit);
 }
 
 }  // namespace vc
@@ -647,16 +648,19 @@ static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
     cudaError_t e = cudaMemsetAsync(fw, 0, sizeof(FrameWork), stream);
     if (e != cudaSuccess) return e;
     const long long tiles = (long long)((L.p->width + 7) / 8) * ((L.local_rows + 3) / 4);
+    if (L.ev[0]) cudaEventRecord(L.ev[0], stream);
     firsthit_kernel<T, OP, INTERP><<<persistent_blocks(firsthit_kernel<T, OP, INTERP>, (tiles + 3) / 4), 128, 0,
                                      stream>>>(*L.p, vol, L.rp, L.occ, L.mx, L.my, L.skip_on,
                                                reinterpret_cast<uchar4*>(L.out), L.local_rows,
                                                reinterpret_cast<unsigned long long*>(L.counters), fw, hits);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    if (L.ev[1]) cudaEventRecord(L.ev[1], stream);
     shade_kernel<T, OP, INTERP><<<persistent_blocks(shade_kernel<T, OP, INTERP>, (tiles + 3) / 4), 128, 0,
                                   stream>>>(*L.p, vol, static_cast<const float4*>(L.grad), L.rp, L.occ, L.mx,
                                             L.my, L.skip_on, reinterpret_cast<uchar4*>(L.out),
                                             reinterpret_cast<unsigned long long*>(L.counters), fw, hits);
+    if (L.ev[2]) cudaEventRecord(L.ev[2], stream);
     return cudaGetLastError();
 }
 

@@ -24,6 +24,7 @@ struct RenderLaunch {
     uint64_t* counters;   // VC_NUM_COUNTERS or nullptr
     void* work;           // frame work counters (FrameWork, zeroed per launch)
     void* hits;           // first-hit queue, >= local_rows * width entries
+    cudaEvent_t ev[3];    // optional: recorded before stage 1, between, after stage 2
 };
 
 cudaError_t launch_raycast(const RenderLaunch& L, cudaStream_t s);

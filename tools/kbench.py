@@ -41,7 +41,7 @@ def main():
     dv = vc.device_volume(vol)
     L = _native.load(build_if_missing=False)
     out = torch.empty((a.height, a.width, 4), dtype=torch.uint8, device="cuda")
-    cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(_native.NUM_COUNTERS, dtype=torch.int64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
     sp = ctypes.c_void_p(stream.cuda_stream)
