@@ -265,6 +265,7 @@ __device__ __forceinline__ uchar4 bg_pixel(const vc_render_params& P) {
 
 // image row of local (packed) row lr under the band partition
 __device__ __forceinline__ int image_row(const vc_render_params& P, int lr) {
+    if (P.band_step == 1) return P.band_first * P.band_rows + lr;  // contiguous rows
     const int band = lr / P.band_rows, within = lr - band * P.band_rows;
     return (P.band_first + band * P.band_step) * P.band_rows + within;
 }
@@ -402,8 +403,10 @@ __device__ __forceinline__ bool shade_and_composite(const Ctx<T>& C, const vc_re
 #endif
 constexpr int READY_NUM = VC_READY_NUM, READY_DEN = 4;
 
-struct HitEntry {  // first-hit queue: pixel + refined parameter t_star
-    double t_star;
+struct HitEntry {  // first-hit queue: pixel, ray and refined parameter t_star
+    double t_star, lim;
+    double d[3];      // ray direction (bit-exact, saves regenerating the ray)
+    double t_enter;
     int lr, px;
 };
 
@@ -524,6 +527,11 @@ __global__ void __launch_bounds__(128, 4) firsthit_kernel(const __grid_constant_
         if (hit) {
             HitEntry e;
             e.t_star = t_star;
+            e.lim = R.lim;
+            e.d[0] = C.rp.d[0];
+            e.d[1] = C.rp.d[1];
+            e.d[2] = C.rp.d[2];
+            e.t_enter = R.t_enter;
             e.lr = lr;
             e.px = px;
             hits[q] = e;
@@ -557,12 +565,12 @@ __global__ void __launch_bounds__(128, 4) shade_kernel(const __grid_constant__ v
     int px = 0, lr = 0;
     bool active = false, done = false;
     for (;;) {
+        // refill: a fresh lane starts "found" at its t_star, so its first
+        // shade joins the other lanes' shades in the single resolve step below
         for (;;) {
             const bool want = !active && !done;
             if (__ballot_sync(FULL, want) == 0) break;
             const unsigned q = warp_ticket(&work->shades, want);
-            bool fresh = false;
-            double t_star = 0.0;
             if (want) {
                 if (q >= total) {
                     done = true;
@@ -570,19 +578,20 @@ __global__ void __launch_bounds__(128, 4) shade_kernel(const __grid_constant__ v
                     const HitEntry e = hits[q];
                     px = e.px;
                     lr = e.lr;
-                    t_star = e.t_star;
-                    start_ray(C, P, px, image_row(P, lr), R);  // a queued ray hit the box
-                    R.base = t_star;
+#pragma unroll
+                    for (int a = 0; a < 3; a++) {
+                        C.rp.d[a] = e.d[a];
+                        C.sk.ib[a] = e.d[a] == 0.0 ? 0.0 : C.rp.s[a] / e.d[a];
+                    }
+                    R.t_enter = e.t_enter;
+                    R.lim = e.lim;
+                    R.base = e.t_star;
                     R.k = 1.0;
-                    fresh = true;
-                }
-            }
-            // the first shade of every fresh ray, all lanes together
-            if (__ballot_sync(FULL, fresh) != 0 && fresh) {
-                uchar4 o;
-                if (shade_and_composite<T, OP, INTERP>(C, P, R, t_star, o, nshade)) {
-                    out[(size_t)lr * P.width + px] = o;
-                } else {
+                    R.acc_r = R.acc_g = R.acc_b = 0.0;
+                    R.remain = 1.0;
+                    R.t_hit = e.t_star;
+                    R.found = true;
+                    R.exhausted = false;
                     active = true;
                 }
             }
