@@ -117,9 +117,9 @@ int validate_dims(int dtype, int nx, int ny, int nz, const double* spacing) {
 
 int finish_create(vc_volume* v) {
     // macrocells over interpolation cells [0, max(n-2,0)] per axis
-    v->mx = std::max(v->nx - 2, 0) / 8 + 1;
-    v->my = std::max(v->ny - 2, 0) / 8 + 1;
-    v->mz = std::max(v->nz - 2, 0) / 8 + 1;
+    v->mx = std::max(v->nx - 2, 0) / vc::MC_EDGE + 1;
+    v->my = std::max(v->ny - 2, 0) / vc::MC_EDGE + 1;
+    v->mz = std::max(v->nz - 2, 0) / vc::MC_EDGE + 1;
     const size_t mc = (size_t)v->mx * v->my * v->mz;
     VC_CUDA(cudaMalloc(&v->d_mm, mc * sizeof(float2)));
     VC_CUDA(cudaMalloc(&v->d_occ, mc));

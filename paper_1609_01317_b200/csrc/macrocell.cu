@@ -24,8 +24,8 @@ __global__ void macrocell_minmax_kernel(const T* __restrict__ vol, int nx, int n
     const int total = mx * my * mz;
     for (int m = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; m < total; m += warps) {
         const int cx = m % mx, cy = (m / mx) % my, cz = m / (mx * my);
-        const int xa = cx * 8, ya = cy * 8, za = cz * 8;
-        const int xb = min(xa + 8, nx - 1), yb = min(ya + 8, ny - 1), zb = min(za + 8, nz - 1);
+        const int xa = cx * MC_EDGE, ya = cy * MC_EDGE, za = cz * MC_EDGE;
+        const int xb = min(xa + MC_EDGE, nx - 1), yb = min(ya + MC_EDGE, ny - 1), zb = min(za + MC_EDGE, nz - 1);
         const int ex = xb - xa + 1, ey = yb - ya + 1, ez = zb - za + 1;
         float lo = FLT_MAX, hi = -FLT_MAX;
         for (int e = lane; e < ex * ey * ez; e += 32) {

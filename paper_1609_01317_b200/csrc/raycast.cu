@@ -29,7 +29,6 @@
 
 namespace vc {
 
-constexpr int MC_SHIFT = 3;  // 8^3 voxel macrocells
 
 struct Skip {
     // per macrocell: 0 = may hold an in-window sample; d >= 1 = every
@@ -473,8 +472,15 @@ __device__ __forceinline__ unsigned warp_ticket(unsigned* ctr, bool want) {
 // queue, misses write the background, and finished lanes take new pixels:
 // the dynamic ray refill of Aila & Laine keeps warps full although
 // neighbouring rays march for very different lengths.
+#ifndef VC_FH_MINB
+#define VC_FH_MINB 6
+#endif
+#ifndef VC_SH_MINB
+#define VC_SH_MINB 5
+#endif
+
 template <typename T, int OP, int INTERP>
-__global__ void __launch_bounds__(128, 4) firsthit_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
+__global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
                                                           RayPos rp0, const uint8_t* __restrict__ dist, int mx,
                                                           int my, int skip_on, uchar4* __restrict__ out,
                                                           int local_rows, unsigned long long* counters,
@@ -550,7 +556,7 @@ __global__ void __launch_bounds__(128, 4) firsthit_kernel(const __grid_constant_
 // samples until early ray termination or the ray leaves the box.  Lanes
 // refill from the queue as their pixel finishes.
 template <typename T, int OP, int INTERP>
-__global__ void __launch_bounds__(128, 4) shade_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
+__global__ void __launch_bounds__(128, VC_SH_MINB) shade_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
                                                        const float4* __restrict__ grad, RayPos rp0,
                                                        const uint8_t* __restrict__ dist, int mx, int my,
                                                        int skip_on, uchar4* __restrict__ out,

@@ -9,6 +9,13 @@
 
 namespace vc {
 
+// macrocell edge = 2^MC_SHIFT voxels (cells [m*E, m*E + E-1], voxels [m*E, m*E + E])
+#ifndef VC_MC_SHIFT
+#define VC_MC_SHIFT 2
+#endif
+constexpr int MC_SHIFT = VC_MC_SHIFT;
+constexpr int MC_EDGE = 1 << MC_SHIFT;
+
 struct RenderLaunch {
     const vc_render_params* p;
     int dtype;
