@@ -175,6 +175,18 @@ __device__ __forceinline__ void grad_from_volume(const float4* __restrict__ G, i
 #undef VC_TRI
 }
 
+#ifdef VC_DEBUG_TAPS
+__device__ unsigned g_debug_taps;
+}  // namespace vc
+extern "C" __attribute__((visibility("default"))) unsigned vc_debug_taps() {
+    unsigned h = 0, z = 0;
+    cudaMemcpyFromSymbol(&h, vc::g_debug_taps, sizeof(unsigned));
+    cudaMemcpyToSymbol(vc::g_debug_taps, &z, sizeof(unsigned));
+    return h;
+}
+namespace vc {
+#endif
+
 struct Rgba {
     double r, g, b, a;
 };
@@ -210,6 +222,9 @@ __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_pa
         val = (INTERP == VC_TRILINEAR) ? gv : sample_any<T, INTERP>(C.v, p[0], p[1], p[2]);
     } else {
         val = sample_any<T, INTERP>(C.v, p[0], p[1], p[2]);
+#ifdef VC_DEBUG_TAPS
+        if (C.grad != nullptr) atomicAdd(&g_debug_taps, 1u);
+#endif
         const double3 gg = grad_taps<T, OP>(C.v, p[0], p[1], p[2]);
         g[0] = gg.x;
         g[1] = gg.y;
@@ -396,15 +411,19 @@ __device__ __forceinline__ bool shade_and_composite(const Ctx<T>& C, const vc_re
 }
 
 // a warp leaves the march loop when READY_NUM / READY_DEN of its live lanes
-// have a hit (or an exhausted ray) to resolve
-#ifndef VC_READY_NUM
-#define VC_READY_NUM 4
+// have a hit (or an exhausted ray) to resolve (first-hit / shade kernel)
+#ifndef VC_FH_READY
+#define VC_FH_READY 4
 #endif
-constexpr int READY_NUM = VC_READY_NUM, READY_DEN = 4;
+#ifndef VC_SH_READY
+#define VC_SH_READY 2
+#endif
+constexpr int READY_DEN = 4;
 
 struct HitEntry {  // first-hit queue: pixel, ray and refined parameter t_star
     double t_star, lim;
     double d[3];      // ray direction (bit-exact, saves regenerating the ray)
+    double ib[3];     // 1 / direction in voxel units (empty-space skipping)
     double t_enter;
     int lr, px;
 };
@@ -523,7 +542,7 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
             const unsigned mneed = __ballot_sync(FULL, need);
             if (mneed == 0) break;
             const unsigned mact = __ballot_sync(FULL, active);
-            if (__popc(mact & ~mneed) * READY_DEN >= __popc(mact) * READY_NUM) break;
+            if (__popc(mact & ~mneed) * READY_DEN >= __popc(mact) * VC_FH_READY) break;
             if (need) march_step<T, INTERP>(C, P, R, nsamp, nskip);
         }
         const bool hit = active && R.found;
@@ -537,6 +556,9 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
             e.d[0] = C.rp.d[0];
             e.d[1] = C.rp.d[1];
             e.d[2] = C.rp.d[2];
+            e.ib[0] = C.sk.ib[0];
+            e.ib[1] = C.sk.ib[1];
+            e.ib[2] = C.sk.ib[2];
             e.t_enter = R.t_enter;
             e.lr = lr;
             e.px = px;
@@ -587,7 +609,7 @@ __global__ void __launch_bounds__(128, VC_SH_MINB) shade_kernel(const __grid_con
 #pragma unroll
                     for (int a = 0; a < 3; a++) {
                         C.rp.d[a] = e.d[a];
-                        C.sk.ib[a] = e.d[a] == 0.0 ? 0.0 : C.rp.s[a] / e.d[a];
+                        C.sk.ib[a] = e.ib[a];
                     }
                     R.t_enter = e.t_enter;
                     R.lim = e.lim;
@@ -608,7 +630,7 @@ __global__ void __launch_bounds__(128, VC_SH_MINB) shade_kernel(const __grid_con
             const unsigned mneed = __ballot_sync(FULL, need);
             if (mneed == 0) break;
             const unsigned mact = __ballot_sync(FULL, active);
-            if (__popc(mact & ~mneed) * READY_DEN >= __popc(mact) * READY_NUM) break;
+            if (__popc(mact & ~mneed) * READY_DEN >= __popc(mact) * VC_SH_READY) break;
             if (need) march_step<T, INTERP>(C, P, R, nsamp, nskip);
         }
         if (active && (R.found || R.exhausted)) {
