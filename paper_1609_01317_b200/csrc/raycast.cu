@@ -492,7 +492,7 @@ __device__ __forceinline__ unsigned warp_ticket(unsigned* ctr, bool want) {
 // the dynamic ray refill of Aila & Laine keeps warps full although
 // neighbouring rays march for very different lengths.
 #ifndef VC_FH_MINB
-#define VC_FH_MINB 6
+#define VC_FH_MINB 8
 #endif
 #ifndef VC_SH_MINB
 #define VC_SH_MINB 5
