@@ -11,13 +11,13 @@
 //   Zucker-Hummel      gx = sum_i,j,k  i / |(i,j,k)| * v                                (:166-176)
 //
 // HBM-bound stencil: 2 B in (u16) + 16 B out per voxel.  Each CTA owns a
-// 32x8 (x,y) column tile and sweeps a z-chunk.  One z-plane of the tile
-// plus a 1-voxel halo is staged in shared memory per step (coalesced
-// rows, zero padding at the faces), each thread reduces the plane to a
-// handful of per-plane partial sums, and the three-plane combination
-// happens in registers as the sweep advances -- every input voxel is read
-// from HBM once (plus the halo), every output float4 is written once with
-// a streaming 16-byte store, a warp storing 512 contiguous bytes.
+// 32x8 (x,y) column tile and a 16-plane z-chunk.  The chunk plus a 1-voxel
+// halo is staged in shared memory in one go (coalesced rows, zero padding
+// at the faces, all loads in flight before one barrier); each thread then
+// sweeps its column, reducing every plane to seven partial sums, and
+// combines three planes in registers -- every input voxel is read from HBM
+// once (plus the halo), every output float4 is written once with a
+// streaming 16-byte store, a warp storing 512 contiguous bytes.
 //
 // Integer grids (u8/u16) accumulate in int32: CD and Sobel3D results are
 // exact integers (|g| <= 44 * 65535 < 2^24), bit-identical to the
@@ -31,6 +31,21 @@ namespace vc {
 
 constexpr int GX = 32, GY = 8, GZC = 16;
 
+// Exact int -> float / double without the XU conversion pipe (profiled at
+// 34% XU on the first version): |v| < 2^22 added into the mantissa of
+// 1.5*2^23, and v + 2^31 into 2^52 (see vc_device.cuh).
+__device__ __forceinline__ float i2f_exact(int v) { return __int_as_float(0x4B400000 + v) - 12582912.0f; }
+template <typename A>
+__device__ __forceinline__ float tof(A v) {
+    if constexpr (sizeof(A) == 4) return i2f_exact(v);
+    else return (float)v;
+}
+template <typename A>
+__device__ __forceinline__ double tod(A v) {
+    if constexpr (sizeof(A) == 4) return biased2d((uint32_t)v + 0x80000000u);
+    else return v;
+}
+
 template <typename A>
 struct Planar {  // per-plane partial sums at one (x, y)
     A d0x, d1x, d0y, d1y, e0, e1, e2;
@@ -39,30 +54,47 @@ struct Planar {  // per-plane partial sums at one (x, y)
 template <typename T, typename A, int OP>
 __global__ void __launch_bounds__(GX* GY) gradient_prepass_kernel(const T* __restrict__ vol, int nx, int ny,
                                                                   int nz, float4* __restrict__ out) {
-    __shared__ A tile[2][GY + 2][GX + 2];
+    // the whole (GZC+2) x (GY+2) x (GX+2) halo'd chunk is staged once: every
+    // thread issues all of its global loads before the single barrier, so
+    // the loads overlap instead of one plane's latency per step
+    constexpr int TW = GX + 2, TH = GY + 2, TD = GZC + 2, TN = TW * TH * TD;
+    __shared__ T tile[TD][TH][TW];
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * GX + tx;
     const int x0 = blockIdx.x * GX, y0 = blockIdx.y * GY;
     const int z0 = blockIdx.z * GZC, z1 = min(z0 + GZC, nz);
     const int x = x0 + tx, y = y0 + ty;
     const size_t plane = (size_t)nx * ny;
 
-    Planar<A> pp{}, pc{}, pn{};
-    for (int zz = z0 - 1; zz <= z1; zz++) {
-        A(*s)[GX + 2] = tile[zz & 1];
-        // stage plane zz of the (GX+2) x (GY+2) halo tile, zero outside the grid
-        for (int e = tid; e < (GX + 2) * (GY + 2); e += GX * GY) {
-            const int ly = e / (GX + 2), lx = e - ly * (GX + 2);
-            const int gx = x0 + lx - 1, gy = y0 + ly - 1;
-            A v = A(0);
-            if (zz >= 0 && zz < nz && gx >= 0 && gx < nx && gy >= 0 && gy < ny)
-                v = (A)__ldg(vol + (size_t)zz * plane + (size_t)gy * nx + gx);
-            s[ly][lx] = v;
+    constexpr int PER = (TN + GX * GY - 1) / (GX * GY);
+    T vals[PER];
+#pragma unroll
+    for (int r = 0; r < PER; r++) {
+        const int e = tid + r * GX * GY;
+        T v = T(0);
+        if (e < TN) {
+            const int lz = e / (TW * TH), rem = e - lz * (TW * TH);
+            const int ly = rem / TW, lx = rem - ly * TW;
+            const int gx = x0 + lx - 1, gy = y0 + ly - 1, gz = z0 + lz - 1;
+            if (gz >= 0 && gz < nz && gx >= 0 && gx < nx && gy >= 0 && gy < ny)
+                v = __ldg(vol + (size_t)gz * plane + (size_t)gy * nx + gx);
         }
-        __syncthreads();
-        const int cx = tx + 1, cy = ty + 1;
-        const A vmm = s[cy - 1][cx - 1], v0m = s[cy - 1][cx], vpm = s[cy - 1][cx + 1];
-        const A vm0 = s[cy][cx - 1], v00 = s[cy][cx], vp0 = s[cy][cx + 1];
-        const A vmp = s[cy + 1][cx - 1], v0p = s[cy + 1][cx], vpp = s[cy + 1][cx + 1];
+        vals[r] = v;
+    }
+#pragma unroll
+    for (int r = 0; r < PER; r++) {
+        const int e = tid + r * GX * GY;
+        if (e < TN) (&tile[0][0][0])[e] = vals[r];
+    }
+    __syncthreads();
+    if (x >= nx || y >= ny) return;
+
+    Planar<A> pp{}, pc{}, pn{};
+    const int cx = tx + 1, cy = ty + 1;
+    auto plane_step = [&](int lz) {
+        const T(*s)[TW] = tile[lz];
+        const A vmm = (A)s[cy - 1][cx - 1], v0m = (A)s[cy - 1][cx], vpm = (A)s[cy - 1][cx + 1];
+        const A vm0 = (A)s[cy][cx - 1], v00 = (A)s[cy][cx], vp0 = (A)s[cy][cx + 1];
+        const A vmp = (A)s[cy + 1][cx - 1], v0p = (A)s[cy + 1][cx], vpp = (A)s[cy + 1][cx + 1];
         pn.d0x = vp0 - vm0;
         pn.d1x = (vpm - vmm) + (vpp - vmp);
         pn.d0y = v0p - v0m;
@@ -70,31 +102,37 @@ __global__ void __launch_bounds__(GX* GY) gradient_prepass_kernel(const T* __res
         pn.e0 = v00;
         pn.e1 = (vm0 + vp0) + (v0m + v0p);
         pn.e2 = (vmm + vpm) + (vmp + vpp);
-        if (zz >= z0 + 1 && x < nx && y < ny) {
+        if (lz >= 2) {
             float4 o;
             if (OP == VC_OP_CENTRAL) {
-                o.x = (float)pc.d0x;
-                o.y = (float)pc.d0y;
-                o.z = (float)(pn.e0 - pp.e0);
+                o.x = tof(pc.d0x);
+                o.y = tof(pc.d0y);
+                o.z = tof(pn.e0 - pp.e0);
             } else if (OP == VC_OP_SOBEL3D) {
                 const A side_x = (A)3 * pp.d0x + pp.d1x + ((A)3 * pn.d0x + pn.d1x);
                 const A side_y = (A)3 * pp.d0y + pp.d1y + ((A)3 * pn.d0y + pn.d1y);
-                o.x = (float)(side_x + ((A)6 * pc.d0x + (A)3 * pc.d1x));
-                o.y = (float)(side_y + ((A)6 * pc.d0y + (A)3 * pc.d1y));
-                o.z = (float)(((A)6 * pn.e0 + (A)3 * pn.e1 + pn.e2) - ((A)6 * pp.e0 + (A)3 * pp.e1 + pp.e2));
+                o.x = tof(side_x + ((A)6 * pc.d0x + (A)3 * pc.d1x));
+                o.y = tof(side_y + ((A)6 * pc.d0y + (A)3 * pc.d1y));
+                o.z = tof(((A)6 * pn.e0 + (A)3 * pn.e1 + pn.e2) - ((A)6 * pp.e0 + (A)3 * pp.e1 + pp.e2));
             } else {
                 const A a1x = pc.d0x, a2x = pc.d1x + (pp.d0x + pn.d0x), a3x = pp.d1x + pn.d1x;
                 const A a1y = pc.d0y, a2y = pc.d1y + (pp.d0y + pn.d0y), a3y = pp.d1y + pn.d1y;
                 const A a1z = pn.e0 - pp.e0, a2z = pn.e1 - pp.e1, a3z = pn.e2 - pp.e2;
-                o.x = (float)dadd(dadd((double)a1x, dmul((double)a2x, INV_SQRT2)), dmul((double)a3x, INV_SQRT3));
-                o.y = (float)dadd(dadd((double)a1y, dmul((double)a2y, INV_SQRT2)), dmul((double)a3y, INV_SQRT3));
-                o.z = (float)dadd(dadd((double)a1z, dmul((double)a2z, INV_SQRT2)), dmul((double)a3z, INV_SQRT3));
+                o.x = (float)dadd(dadd(tod(a1x), dmul(tod(a2x), INV_SQRT2)), dmul(tod(a3x), INV_SQRT3));
+                o.y = (float)dadd(dadd(tod(a1y), dmul(tod(a2y), INV_SQRT2)), dmul(tod(a3y), INV_SQRT3));
+                o.z = (float)dadd(dadd(tod(a1z), dmul(tod(a2z), INV_SQRT2)), dmul(tod(a3z), INV_SQRT3));
             }
-            o.w = (float)pc.e0;
-            __stcs(out + (size_t)(zz - 1) * plane + (size_t)y * nx + x, o);
+            o.w = tof(pc.e0);
+            __stcs(out + (size_t)(z0 + lz - 2) * plane + (size_t)y * nx + x, o);
         }
         pp = pc;
         pc = pn;
+    };
+    if (z1 - z0 == GZC) {  // full chunk: unrolled sweep (independent planes overlap)
+#pragma unroll
+        for (int lz = 0; lz < GZC + 2; lz++) plane_step(lz);
+    } else {
+        for (int lz = 0; lz < z1 - z0 + 2; lz++) plane_step(lz);
     }
 }
 
