@@ -17,6 +17,7 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <vector>
 
 #include "vc_internal.h"
 
@@ -28,12 +29,21 @@ struct vc_volume {
     void* d_data = nullptr;
     size_t bytes = 0;
     float2* d_mm = nullptr;
-    uint8_t* d_occ = nullptr;      // macrocell distance field of the last window
-    uint8_t* d_occ_tmp = nullptr;
+    // macrocell distance fields, one per threshold window seen (LRU, at most
+    // MAX_FIELDS); `ready` orders the build before renders on other streams,
+    // `last_use` guards reuse of an evicted slot
+    struct WindowField {
+        double lo = 0.0, hi = 0.0;
+        uint8_t* dist = nullptr;
+        uint8_t* tmp = nullptr;
+        cudaEvent_t ready = nullptr, last_use = nullptr;
+        uint64_t stamp = 0;
+    };
+    std::vector<WindowField> fields;
+    uint64_t clock = 0;
     int mx = 0, my = 0, mz = 0;
-    bool occ_valid = false;
-    double occ_lo = 0.0, occ_hi = 0.0;
     float4* d_grad[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t grad_ready[3] = {nullptr, nullptr, nullptr};
     uint8_t* d_scratch = nullptr;
     size_t scratch_bytes = 0;
     uint64_t* d_counters = nullptr;
@@ -122,8 +132,6 @@ int finish_create(vc_volume* v) {
     v->mz = std::max(v->nz - 2, 0) / vc::MC_EDGE + 1;
     const size_t mc = (size_t)v->mx * v->my * v->mz;
     VC_CUDA(cudaMalloc(&v->d_mm, mc * sizeof(float2)));
-    VC_CUDA(cudaMalloc(&v->d_occ, mc));
-    VC_CUDA(cudaMalloc(&v->d_occ_tmp, mc));
     VC_CUDA(cudaMalloc(&v->d_counters, VC_NUM_COUNTERS * sizeof(uint64_t)));
     VC_CUDA(cudaStreamCreateWithFlags(&v->host_stream, cudaStreamNonBlocking));
     VC_CUDA(cudaEventCreate(&v->ev0));
@@ -139,8 +147,14 @@ void release(vc_volume* v) {
     DeviceGuard g(v->device);
     cudaFree(v->d_data);
     cudaFree(v->d_mm);
-    cudaFree(v->d_occ);
-    cudaFree(v->d_occ_tmp);
+    for (auto& f : v->fields) {
+        cudaFree(f.dist);
+        cudaFree(f.tmp);
+        if (f.ready) cudaEventDestroy(f.ready);
+        if (f.last_use) cudaEventDestroy(f.last_use);
+    }
+    for (auto& e : v->grad_ready)
+        if (e) cudaEventDestroy(e);
     for (auto& p : v->d_grad) cudaFree(p);
     cudaFree(v->d_scratch);
     cudaFree(v->d_counters);
@@ -194,7 +208,10 @@ int create_common(int device, const void* src, cudaMemcpyKind kind, int dtype, i
 }
 
 int ensure_grad(vc_volume* v, int op, cudaStream_t s) {
-    if (v->d_grad[op]) return VC_OK;
+    if (v->d_grad[op]) {
+        VC_CUDA(cudaStreamWaitEvent(s, v->grad_ready[op], 0));  // built on another stream
+        return VC_OK;
+    }
     float4* g = nullptr;
     cudaError_t e = cudaMalloc(&g, (size_t)v->nx * v->ny * v->nz * sizeof(float4));
     if (e != cudaSuccess) return fail(VC_ERR_NOMEM, std::string("cudaMalloc(gradient volume): ") + cudaGetErrorString(e));
@@ -204,6 +221,44 @@ int ensure_grad(vc_volume* v, int op, cudaStream_t s) {
         return cuda_fail(e, "gradient pre-pass launch");
     }
     v->d_grad[op] = g;
+    if (!v->grad_ready[op]) VC_CUDA(cudaEventCreateWithFlags(&v->grad_ready[op], cudaEventDisableTiming));
+    VC_CUDA(cudaEventRecord(v->grad_ready[op], s));
+    return VC_OK;
+}
+
+constexpr size_t MAX_FIELDS = 8;
+
+// distance field of window [lo, hi], built on stream s if not cached
+int window_field(vc_volume* v, double lo, double hi, cudaStream_t s, vc_volume::WindowField** out) {
+    v->clock++;
+    for (auto& f : v->fields)
+        if (f.lo == lo && f.hi == hi) {
+            f.stamp = v->clock;
+            VC_CUDA(cudaStreamWaitEvent(s, f.ready, 0));
+            *out = &f;
+            return VC_OK;
+        }
+    vc_volume::WindowField* f = nullptr;
+    if (v->fields.size() < MAX_FIELDS) {
+        v->fields.emplace_back();
+        f = &v->fields.back();
+        const size_t mc = (size_t)v->mx * v->my * v->mz;
+        VC_CUDA(cudaMalloc(&f->dist, mc));
+        VC_CUDA(cudaMalloc(&f->tmp, mc));
+        VC_CUDA(cudaEventCreateWithFlags(&f->ready, cudaEventDisableTiming));
+        VC_CUDA(cudaEventCreateWithFlags(&f->last_use, cudaEventDisableTiming));
+    } else {
+        f = &v->fields[0];
+        for (auto& g : v->fields)
+            if (g.stamp < f->stamp) f = &g;
+        VC_CUDA(cudaEventSynchronize(f->last_use));  // renders still reading the evicted field
+    }
+    f->lo = lo;
+    f->hi = hi;
+    f->stamp = v->clock;
+    VC_CUDA(vc::launch_occupancy(v->d_mm, v->mx, v->my, v->mz, lo, hi, f->dist, f->tmp, s));
+    VC_CUDA(cudaEventRecord(f->ready, s));
+    *out = f;
     return VC_OK;
 }
 
@@ -264,15 +319,14 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
     }
     L.mx = v->mx;
     L.my = v->my;
-    L.occ = v->d_occ;
+    L.occ = nullptr;
     const bool zero_in_window = p->t_low <= 0.0 && 0.0 <= p->t_high;
     L.skip_on = (p->skip_empty && !zero_in_window) ? 1 : 0;
-    if (L.skip_on && !(v->occ_valid && v->occ_lo == p->t_low && v->occ_hi == p->t_high)) {
-        VC_CUDA(vc::launch_occupancy(v->d_mm, v->mx, v->my, v->mz, p->t_low, p->t_high, v->d_occ,
-                                     v->d_occ_tmp, s));
-        v->occ_valid = true;
-        v->occ_lo = p->t_low;
-        v->occ_hi = p->t_high;
+    vc_volume::WindowField* field = nullptr;
+    if (L.skip_on) {
+        int rc = window_field(v, p->t_low, p->t_high, s, &field);
+        if (rc) return rc;
+        L.occ = field->dist;
     }
     L.grad = nullptr;
     if (p->grad_source == VC_GRAD_VOLUME) {
@@ -283,6 +337,7 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
     if (d_counters) VC_CUDA(cudaMemsetAsync(d_counters, 0, VC_NUM_COUNTERS * sizeof(uint64_t), s));
     if (local_rows == 0) return VC_OK;
     VC_CUDA(vc::launch_raycast(L, s));
+    if (field) VC_CUDA(cudaEventRecord(field->last_use, s));
     return VC_OK;
 }
 

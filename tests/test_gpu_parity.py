@@ -260,3 +260,25 @@ def test_band_partition_reassembles_whole_frame(ct512):
             torch.cuda.synchronize()
             img[rows] = out.cpu().numpy()
         assert np.array_equal(img, whole), (band_rows, owners)
+
+
+def test_render_sequence_matches_render_frame():
+    vol = phantoms.ct_phantom(96)
+    frames = [phantoms.scene_c3(vol, width=160, height=90, azimuth=float(a)) for a in (0, 33, 71, 150, 299)]
+    want = [vc.render_frame(vol, sc, st).pixels.copy() for sc, st in frames]
+    got = [(fb.pixels.copy(), fb.sample_count) for fb in vc.render_sequence(vol, frames, depth=2)]
+    assert len(got) == len(want)
+    for (g, cnt), w in zip(got, want):
+        assert np.array_equal(g, w) and cnt > 0
+
+
+def test_window_changes_between_frames_use_their_own_distance_fields():
+    """Several threshold windows in flight on one volume (the distance-field
+    cache is keyed by window): every frame stays bit-exact vs the oracle."""
+    vol = phantoms.ct_phantom(64)
+    base_sc, st = phantoms.scene_c3(vol, width=64, height=48, azimuth=20.0, mode="surface")
+    for lo in (500.0, 950.0, 1200.0, 500.0, 1290.0, 960.0, 400.0, 600.0, 700.0, 800.0, 500.0):
+        sc = vc.Scene(camera=base_sc.camera, light=base_sc.light, window=vc.ThresholdWindow(lo, 4095.0))
+        want, _ = oracle.render(vol.as_array(), vol.spacing, spec_of((sc, st)))
+        fb = vc.render_frame(vol, sc, st)
+        assert np.array_equal(fb.pixels, want), lo
