@@ -21,8 +21,9 @@ template <typename T, int OP>
 __global__ void gradient_points_kernel(Vol<T> v, const double* __restrict__ pts, int64_t n, double* out) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    double g[3];
-    grad_raw<T, OP>(v, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], g);
+    double g[3], center;
+    if (!grad_raw_shared<T, OP>(v, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], g, center))
+        grad_raw<T, OP>(v, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], g);
     out[3 * i] = g[0];
     out[3 * i + 1] = g[1];
     out[3 * i + 2] = g[2];

@@ -195,11 +195,14 @@ struct Rgba {
 // when shading from the gradient volume (boundary band only) and keeping
 // it out of the march loop keeps the hot code small (the first profile
 // showed instruction-cache stalls).
+// .w of the result: sample_trilinear at the point when the shared-footprint
+// path applied (NaN otherwise)
 template <typename T, int OP>
-__device__ __noinline__ double3 grad_taps(Vol<T> v, double x, double y, double z) {
-    double g[3];
+__device__ __noinline__ double4 grad_taps(Vol<T> v, double x, double y, double z) {
+    double g[3], center;
+    if (grad_raw_shared<T, OP>(v, x, y, z, g, center)) return make_double4(g[0], g[1], g[2], center);
     grad_raw<T, OP>(v, x, y, z, g);
-    return make_double3(g[0], g[1], g[2]);
+    return make_double4(g[0], g[1], g[2], __longlong_as_double(0x7ff8000000000000LL));
 }
 
 // _kernels.py:528-579
@@ -221,14 +224,15 @@ __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_pa
         grad_from_volume(C.grad, C.v.nx, C.v.ny, p, g, gv);
         val = (INTERP == VC_TRILINEAR) ? gv : sample_any<T, INTERP>(C.v, p[0], p[1], p[2]);
     } else {
-        val = sample_any<T, INTERP>(C.v, p[0], p[1], p[2]);
 #ifdef VC_DEBUG_TAPS
         if (C.grad != nullptr) atomicAdd(&g_debug_taps, 1u);
 #endif
-        const double3 gg = grad_taps<T, OP>(C.v, p[0], p[1], p[2]);
+        const double4 gg = grad_taps<T, OP>(C.v, p[0], p[1], p[2]);
         g[0] = gg.x;
         g[1] = gg.y;
         g[2] = gg.z;
+        // the footprint's centre is sample_trilinear(p) (bit-identical)
+        val = (INTERP == VC_TRILINEAR && gg.w == gg.w) ? gg.w : sample_any<T, INTERP>(C.v, p[0], p[1], p[2]);
     }
     double u[3];
     normalize3(g, u);

@@ -330,6 +330,98 @@ __device__ __forceinline__ void grad_raw(const Vol<T>& v, double x, double y, do
     g[2] = gz;
 }
 
+// grad_raw for the common interior case, sharing one 4x4x4 voxel footprint
+// between the 26 (6) taps.  When every tap coordinate x+i is exact -- x >= 1,
+// x+1 < n-1 and x+1 does not cross a binade with rounding -- all taps have
+// the fractions of x and cells shifted by i, none is clamped and all are in
+// range, so each tap's x-lerps are the shared X[j][k] below, its y-lerps the
+// shared Y, its z-lerp Z: the same float64 operations on the same operands
+// as grad_raw / sample_trilinear, accumulated in the same i->j->k order, so
+// the result is bit-identical (3.5x fewer loads and FP64 ops).  `center`
+// receives sample_trilinear(x, y, z).  Returns false when the fast path does
+// not apply (the caller then uses grad_raw).
+template <typename T, int OP>
+__device__ __forceinline__ bool grad_raw_shared(const Vol<T>& v, double x, double y, double z, double g[3],
+                                                double& center) {
+    const double xp = dadd(x, 1.0), yp = dadd(y, 1.0), zp = dadd(z, 1.0);
+    if (!(x >= 1.0 && xp < v.mx && dsub(xp, x) == 1.0 && y >= 1.0 && yp < v.my && dsub(yp, y) == 1.0 &&
+          z >= 1.0 && zp < v.mz && dsub(zp, z) == 1.0))
+        return false;
+    double r;
+    const int i0 = floor_pos(x, r);
+    const double fx = dsub(x, r);
+    const int j0 = floor_pos(y, r);
+    const double fy = dsub(y, r);
+    const int k0 = floor_pos(z, r);
+    const double fz = dsub(z, r);
+    const uint32_t sy = (uint32_t)v.nx, sz = (uint32_t)v.nx * (uint32_t)v.ny;
+    // corner (i0-1, j0-1, k0-1) of the footprint
+    const T* b = v.data + (((uint32_t)(k0 - 1) * (uint32_t)v.ny + (uint32_t)(j0 - 1)) * (uint32_t)v.nx +
+                           (uint32_t)(i0 - 1));
+    if (OP == VC_OP_CENTRAL) {
+        // tap at cell offset (di, dj, dk): trilinear over footprint cell (1+di, 1+dj, 1+dk)
+        auto tri = [&](int di, int dj, int dk) {
+            const T* c = b + (uint32_t)(1 + dk) * sz + (uint32_t)(1 + dj) * sy + (uint32_t)(1 + di);
+            const double x00 = lerp_vox<T>(ldv(c), ldv(c + 1), fx);
+            const double x10 = lerp_vox<T>(ldv(c + sy), ldv(c + sy + 1), fx);
+            const double x01 = lerp_vox<T>(ldv(c + sz), ldv(c + sz + 1), fx);
+            const double x11 = lerp_vox<T>(ldv(c + sz + sy), ldv(c + sz + sy + 1), fx);
+            return lerp(lerp(x00, x10, fy), lerp(x01, x11, fy), fz);
+        };
+        g[0] = dsub(tri(1, 0, 0), tri(-1, 0, 0));
+        g[1] = dsub(tri(0, 1, 0), tri(0, -1, 0));
+        g[2] = dsub(tri(0, 0, 1), tri(0, 0, -1));
+        center = tri(0, 0, 0);
+        return true;
+    }
+    double gx = 0.0, gy = 0.0, gz = 0.0;
+#pragma unroll
+    for (int i = -1; i < 2; i++) {
+        double X[4][4];  // [row j0-1+jj][slice k0-1+kk], x-lerp over cells i0+i, i0+i+1
+#pragma unroll
+        for (int kk = 0; kk < 4; kk++)
+#pragma unroll
+            for (int jj = 0; jj < 4; jj++) {
+                const T* c = b + (uint32_t)kk * sz + (uint32_t)jj * sy + (uint32_t)(i + 1);
+                X[jj][kk] = lerp_vox<T>(ldv(c), ldv(c + 1), fx);
+            }
+        double Y[3][4];  // tap row j: lerp(X[j+1], X[j+2], fy)
+#pragma unroll
+        for (int j = 0; j < 3; j++)
+#pragma unroll
+            for (int kk = 0; kk < 4; kk++) Y[j][kk] = lerp(X[j][kk], X[j + 1][kk], fy);
+#pragma unroll
+        for (int j = -1; j < 2; j++) {
+#pragma unroll
+            for (int k = -1; k < 2; k++) {
+                const double s = lerp(Y[j + 1][k + 1], Y[j + 1][k + 2], fz);
+                if (i == 0 && j == 0 && k == 0) {
+                    center = s;
+                    continue;
+                }
+                double wx, wy, wz;
+                if (OP == VC_OP_SOBEL3D) {
+                    wx = (double)i * smooth_weight(j, k);
+                    wy = (double)j * smooth_weight(i, k);
+                    wz = (double)k * smooth_weight(i, j);
+                } else {
+                    const double inv = zh_inv(i, j, k);
+                    wx = (double)i * inv;
+                    wy = (double)j * inv;
+                    wz = (double)k * inv;
+                }
+                if (i != 0) gx = dadd(gx, dmul(wx, s));
+                if (j != 0) gy = dadd(gy, dmul(wy, s));
+                if (k != 0) gz = dadd(gz, dmul(wz, s));
+            }
+        }
+    }
+    g[0] = gx;
+    g[1] = gy;
+    g[2] = gz;
+    return true;
+}
+
 // _kernels.py:180-185
 __device__ __forceinline__ void normalize3(const double g[3], double u[3]) {
     const double n = __dsqrt_rn(dadd(dadd(dmul(g[0], g[0]), dmul(g[1], g[1])), dmul(g[2], g[2])));
