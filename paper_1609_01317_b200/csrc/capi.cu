@@ -42,6 +42,7 @@ struct vc_volume {
     std::vector<WindowField> fields;
     uint64_t clock = 0;
     int mx = 0, my = 0, mz = 0;
+    double vmin = 0.0, vmax = 0.0;  // value range (from the macrocell grid)
     float4* d_grad[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t grad_ready[3] = {nullptr, nullptr, nullptr};
     uint8_t* d_scratch = nullptr;
@@ -138,7 +139,16 @@ int finish_create(vc_volume* v) {
     VC_CUDA(cudaEventCreate(&v->ev1));
     VC_CUDA(vc::launch_macrocell_minmax(v->dtype, v->d_data, v->nx, v->ny, v->nz, v->d_mm, v->mx, v->my,
                                         v->mz, v->host_stream));
+    std::vector<float2> mm(mc);
+    VC_CUDA(cudaMemcpyAsync(mm.data(), v->d_mm, mc * sizeof(float2), cudaMemcpyDeviceToHost, v->host_stream));
     VC_CUDA(cudaStreamSynchronize(v->host_stream));
+    double lo = mm[0].x, hi = mm[0].y;
+    for (const auto& r : mm) {
+        lo = std::min(lo, (double)r.x);
+        hi = std::max(hi, (double)r.y);
+    }
+    v->vmin = lo;
+    v->vmax = hi;
     return VC_OK;
 }
 
@@ -298,6 +308,8 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
     L.nx = v->nx;
     L.ny = v->ny;
     L.nz = v->nz;
+    L.amax = std::max(std::fabs(v->vmin), std::fabs(v->vmax));
+    if (!std::isfinite(L.amax)) L.amax = -1.0;  // no float32 pre-test
     L.rp = make_raypos(v);
     L.out = d_rgba;
     L.local_rows = local_rows;

@@ -39,6 +39,7 @@ struct Skip {
     double ib[3];      // 1 / (ray direction in voxel units per unit t)
     double inv_coarse;
     bool on;
+    WinF win;          // float32 pre-test thresholds of the window
 };
 
 template <typename T>
@@ -83,22 +84,26 @@ __device__ __forceinline__ double skip_to(double t, double k, double base, const
     return kn;
 }
 
+__device__ __forceinline__ bool in_window(const vc_render_params& P, double v) {
+    return P.t_low <= v && v <= P.t_high;
+}
+
 __device__ __forceinline__ uint32_t macro_index(const Skip& sk, const Loc& L) {
     return ((uint32_t)(L.k >> MC_SHIFT) * (uint32_t)sk.my + (uint32_t)(L.j >> MC_SHIFT)) * (uint32_t)sk.mx +
            (uint32_t)(L.i >> MC_SHIFT);
 }
 
-// One lattice sample of the march: returns true and the value when it must
-// be evaluated (the reference's sample_any at p), false when empty-space
-// skipping proves it out of window, in which case k has been advanced.
+// One lattice sample of the march: -1 when empty-space skipping proves it
+// out of window (k has been advanced, no fetch), else whether the
+// reference's sample_any at p lies in the threshold window (0 / 1).
 template <typename T, int INTERP>
-__device__ __forceinline__ bool march_sample(const Ctx<T>& C, const double p[3], double t, double& k,
-                                             double base, unsigned& nskip, double& val) {
+__device__ __forceinline__ int march_sample(const Ctx<T>& C, const vc_render_params& P, const double p[3],
+                                            double t, double& k, double base, unsigned& nskip) {
     if (INTERP != VC_TRILINEAR) {
         if (C.sk.on && !in_range(C.v, p[0], p[1], p[2])) {  // reads 0, outside the window
             k += 1.0;
             nskip += 1;
-            return false;
+            return -1;
         }
         if (C.sk.on) {
             Loc L;
@@ -109,11 +114,10 @@ __device__ __forceinline__ bool march_sample(const Ctx<T>& C, const double p[3],
                 const double kn = skip_to(t, k, base, C.sk, p, c, d);
                 nskip += (unsigned)__double2uint_rz(kn - k);
                 k = kn;
-                return false;
+                return -1;
             }
         }
-        val = sample_any<T, INTERP>(C.v, p[0], p[1], p[2]);
-        return true;
+        return in_window(P, sample_any<T, INTERP>(C.v, p[0], p[1], p[2])) ? 1 : 0;
     }
     Loc L;
     const bool inr = locate(C.v, p, L);
@@ -121,7 +125,7 @@ __device__ __forceinline__ bool march_sample(const Ctx<T>& C, const double p[3],
         if (!inr) {  // reads 0, and 0 is outside the window when skipping is on
             k += 1.0;
             nskip += 1;
-            return false;
+            return -1;
         }
         const int d = __ldg(C.sk.dist + macro_index(C.sk, L));
         if (d != 0) {
@@ -129,19 +133,20 @@ __device__ __forceinline__ bool march_sample(const Ctx<T>& C, const double p[3],
             const double kn = skip_to(t, k, base, C.sk, p, c, d);
             nskip += (unsigned)__double2uint_rz(kn - k);
             k = kn;
-            return false;
+            return -1;
         }
     }
-    val = inr ? trilinear_at(C.v, L) : 0.0;
-    return true;
+    if (!inr) return in_window(P, 0.0) ? 1 : 0;
+    return in_window_trilinear(C.v, L, P.t_low, P.t_high, C.sk.win) ? 1 : 0;
 }
 
-// sample_any at p (fine scan, bisection)
+// is sample_any at p in the window? (fine scan, bisection)
 template <typename T, int INTERP>
-__device__ __forceinline__ double sample_at(const Ctx<T>& C, const double p[3]) {
-    if (INTERP != VC_TRILINEAR) return sample_any<T, INTERP>(C.v, p[0], p[1], p[2]);
+__device__ __forceinline__ bool window_at(const Ctx<T>& C, const vc_render_params& P, const double p[3]) {
+    if (INTERP != VC_TRILINEAR) return in_window(P, sample_any<T, INTERP>(C.v, p[0], p[1], p[2]));
     Loc L;
-    return locate(C.v, p, L) ? trilinear_at(C.v, L) : 0.0;
+    if (!locate(C.v, p, L)) return in_window(P, 0.0);
+    return in_window_trilinear(C.v, L, P.t_low, P.t_high, C.sk.win);
 }
 
 // Trilinear interpolation of the packed gradient volume at an interior
@@ -256,10 +261,6 @@ __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_pa
     return out;
 }
 
-__device__ __forceinline__ bool in_window(const vc_render_params& P, double v) {
-    return P.t_low <= v && v <= P.t_high;
-}
-
 // Per-lane ray state of the persistent kernel.  A pixel is traced as a
 // sequence of "events"; one event = march the lattice base + k*coarse to
 // the next in-window sample (+ fine backward scan and bisection for the
@@ -330,11 +331,11 @@ __device__ __forceinline__ void march_step(const Ctx<T>& C, const vc_render_para
     }
     double p[3];
     C.rp.at(t, p);
-    double val;
-    if (!march_sample<T, INTERP>(C, p, t, R.k, R.base, nskip, val)) return;
+    const int w = march_sample<T, INTERP>(C, P, p, t, R.k, R.base, nskip);
+    if (w < 0) return;
     nsamp++;
     R.k += 1.0;
-    if (in_window(P, val)) {
+    if (w) {
         R.found = true;
         R.t_hit = t;
     }
@@ -358,8 +359,7 @@ __device__ __forceinline__ double refine_hit(const Ctx<T>& C, const vc_render_pa
         double b[3];
         C.rp.at(tb, b);
         nsamp++;
-        const double vb = sample_at<T, INTERP>(C, b);
-        if (!in_window(P, vb)) {
+        if (!window_at<T, INTERP>(C, P, b)) {
             t_in = dsub(t, dmul(j - 1.0, fine));
             t_before = tb;
             bracket = true;
@@ -374,8 +374,7 @@ __device__ __forceinline__ double refine_hit(const Ctx<T>& C, const vc_render_pa
             double p[3];
             C.rp.at(tm, p);
             nsamp++;
-            const double val = sample_at<T, INTERP>(C, p);
-            if (in_window(P, val)) ta = tm;
+            if (window_at<T, INTERP>(C, P, p)) ta = tm;
             else tb = tm;
         }
         tcur = ta;
@@ -454,6 +453,7 @@ __device__ __forceinline__ void init_ctx(Ctx<T>& C, const vc_render_params& P, c
     C.sk.my = my;
     C.sk.on = skip_on != 0;
     C.sk.inv_coarse = 1.0 / P.coarse;
+    C.sk.win = make_winf(P.t_low, P.t_high, vol.amax);
 }
 
 __device__ __forceinline__ void commit_counters(unsigned long long* counters, int stage, unsigned nsamp,
@@ -683,7 +683,7 @@ static unsigned persistent_blocks(K kernel, long long max_useful) {
 
 template <typename T, int OP, int INTERP>
 static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
-    const Vol<T> vol = make_vol(static_cast<const T*>(L.data), L.nx, L.ny, L.nz);
+    const Vol<T> vol = make_vol(static_cast<const T*>(L.data), L.nx, L.ny, L.nz, L.amax);
     FrameWork* fw = reinterpret_cast<FrameWork*>(L.work);
     HitEntry* hits = reinterpret_cast<HitEntry*>(L.hits);
     cudaError_t e = cudaMemsetAsync(fw, 0, sizeof(FrameWork), stream);

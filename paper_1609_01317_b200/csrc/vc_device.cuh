@@ -44,11 +44,14 @@ struct Vol {
     // n-1 and max(n-2, 0) as doubles: range checks and cell clamps without
     // an I2F.F64 per sample (make_vol fills them)
     double mx, my, mz, cx, cy, cz;
+    // max |voxel value| (bounds the float32 pre-test error); <= 0: unknown
+    double amax;
 };
 
 template <typename T>
-__host__ __device__ inline Vol<T> make_vol(const T* data, int nx, int ny, int nz) {
+__host__ __device__ inline Vol<T> make_vol(const T* data, int nx, int ny, int nz, double amax = -1.0) {
     Vol<T> v;
+    v.amax = amax;
     v.data = data;
     v.nx = nx;
     v.ny = ny;
@@ -226,6 +229,70 @@ __device__ __forceinline__ double trilinear_at(const Vol<T>& v, const Loc& L) {
     const double y0 = lerp(x00, x10, L.fy);
     const double y1 = lerp(x01, x11, L.fy);
     return lerp(y0, y1, L.fz);
+}
+
+// ---- in-window test with a float32 pre-test -------------------------------
+// March, fine-scan, bisection and composite-march samples are only ever
+// compared with the threshold window.  The trilinear value is first formed
+// in float32 from the same eight voxels and the float64 fractions; its
+// error is below E = amax * 2^-16 (corners exact in float32, each of the
+// three lerp levels adds at most a few ulp of amax -- about 34 * 2^-24 *
+// amax in total, so E has a 4x margin).  Only a value within E of a
+// threshold is re-evaluated with the reference's float64 cascade, so every
+// decision equals the reference's.
+struct WinF {
+    float lo_out, lo_in, hi_in, hi_out;  // v < lo_out or > hi_out: out; lo_in <= v <= hi_in: in
+};
+
+__host__ __device__ inline double prefilter_error(double amax) { return amax > 0.0 ? amax * 0x1p-16 + 1e-30 : 1e300; }
+
+__device__ __forceinline__ WinF make_winf(double t_low, double t_high, double amax) {
+    const double e = prefilter_error(amax);
+    WinF w;
+    if (e > 1e200) {  // unknown range: always take the exact path
+        w.lo_out = -INFINITY;
+        w.hi_out = INFINITY;
+        w.lo_in = INFINITY;
+        w.hi_in = -INFINITY;
+        return w;
+    }
+    w.lo_out = __double2float_rd(t_low - e);
+    w.lo_in = __double2float_ru(t_low + e);
+    w.hi_in = __double2float_rd(t_high - e);
+    w.hi_out = __double2float_ru(t_high + e);
+    return w;
+}
+
+template <typename T>
+__device__ __forceinline__ float vox_f32(T c) {
+    if constexpr (VoxelBits<T>::integral) return __int_as_float(0x4B000000 | (int)c) - 8388608.0f;
+    else return (float)c;
+}
+
+template <typename T>
+__device__ __forceinline__ bool in_window_trilinear(const Vol<T>& v, const Loc& L, double t_low, double t_high,
+                                                    const WinF& w) {
+    const uint32_t sx = L.i + 1 < v.nx ? 1u : 0u;
+    const uint32_t sy = L.j + 1 < v.ny ? (uint32_t)v.nx : 0u;
+    const uint32_t sz = L.k + 1 < v.nz ? (uint32_t)v.nx * (uint32_t)v.ny : 0u;
+    const T* b = v.data + (((uint32_t)L.k * (uint32_t)v.ny + (uint32_t)L.j) * (uint32_t)v.nx + (uint32_t)L.i);
+    const T c000 = ldv(b), c100 = ldv(b + sx), c010 = ldv(b + sy), c110 = ldv(b + sy + sx);
+    const T c001 = ldv(b + sz), c101 = ldv(b + sz + sx), c011 = ldv(b + sz + sy),
+            c111 = ldv(b + sz + sy + sx);
+    const float fx = __double2float_rn(L.fx), fy = __double2float_rn(L.fy), fz = __double2float_rn(L.fz);
+    auto l32 = [](float a, float bb, float t) { return __fmaf_rn(bb - a, t, a); };
+    const float y0 = l32(l32(vox_f32(c000), vox_f32(c100), fx), l32(vox_f32(c010), vox_f32(c110), fx), fy);
+    const float y1 = l32(l32(vox_f32(c001), vox_f32(c101), fx), l32(vox_f32(c011), vox_f32(c111), fx), fy);
+    const float v32 = l32(y0, y1, fz);
+    if (v32 < w.lo_out || v32 > w.hi_out) return false;
+    if (v32 >= w.lo_in && v32 <= w.hi_in) return true;
+    // ambiguous: the reference's float64 cascade on the same corners
+    const double x00 = lerp_vox<T>(c000, c100, L.fx);
+    const double x10 = lerp_vox<T>(c010, c110, L.fx);
+    const double x01 = lerp_vox<T>(c001, c101, L.fx);
+    const double x11 = lerp_vox<T>(c011, c111, L.fx);
+    const double val = lerp(lerp(x00, x10, L.fy), lerp(x01, x11, L.fy), L.fz);
+    return t_low <= val && val <= t_high;
 }
 
 // _kernels.py:67-72

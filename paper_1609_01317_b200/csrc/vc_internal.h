@@ -21,6 +21,7 @@ struct RenderLaunch {
     int dtype;
     const void* data;
     int nx, ny, nz;
+    double amax;          // max |voxel value| (float32 pre-test bound)
     const void* grad;     // packed float4 gradient volume or nullptr (taps)
     RayPos rp;            // spacing / reciprocal / pow2 filled in; o, d per pixel
     const uint8_t* occ;   // macrocell occupancy for the current window
