@@ -340,6 +340,27 @@ def run_ours(args):
     w_frame = bf[0] + bf[1]  # ray samples incl. each shade's value sample
     k_frame = bf[1]
 
+    # device fps of the bit-exact float64 configuration (reference taps for
+    # the shading gradient) on the same frames, same timing rules
+    exact = None
+    if args.grad != "taps":
+        ms_ex = []
+        for k in range(min(args.steps, 50)):
+            sc, st = frame(args.warmup + k)
+            P = render_params(vol, sc, replace(st, gradient_source="taps"), band_rows=plan.band_rows,
+                              band_first=rank, band_step=world)
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _native.check(L.vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(local_buf.data_ptr()),
+                                      None, sp))
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ms_ex.append(e0.elapsed_time(e1))
+        exact = {"fps": 1000.0 / float(np.mean(ms_ex)), "ms_per_step": float(np.mean(ms_ex)),
+                 "gradient_source": "taps",
+                 "parity": "bit-exact vs the reference (tests/test_gpu_parity.py)"}
+
     # executed work and per-stage device time of the timed configuration
     stage = np.zeros(2)
     ce = np.zeros(_native.NUM_COUNTERS)
@@ -456,6 +477,7 @@ def run_ours(args):
                              "of the work counters)",
         "clocks": clk.summary(),
         "parity": parity,
+        "exact_fp64_path": exact,
         "wall_s_timed_region": t_wall,
     }
     print(json.dumps(line), flush=True)
