@@ -102,7 +102,30 @@ typedef struct vc_render_params {
     int32_t skip_empty;                 /* macrocell empty-space skipping; output-neutral,
                                            replaces the octree (use_octree, raycast.py:187) */
     int32_t grad_source;                /* vc_grad_source */
+    /* adaptive stride (use_adaptive, _kernels.py:437-463): after an
+     * out-of-window first-hit sample inside an octree leaf whose padded
+     * range spans < detail_eps, advance up to adapt_jump lattice steps
+     * (never past the leaf).  Needs vc_volume_set_octree; forces
+     * skip_empty off (the stride depends on the exact lattice sequence). */
+    int32_t use_adaptive, adapt_jump;
+    double detail_eps;
 } vc_render_params;
+
+/* Min/max octree in level-grid form (see paper_1609_01317_b200/octree.py):
+ * the boxes of depth L are the product of per-axis interval lists; per box
+ * a state (0 absent, 1 internal, 2 leaf) and the padded value range.  All
+ * arrays are host memory, copied by vc_volume_set_octree. */
+typedef struct vc_octree_desc {
+    int32_t levels;
+    const int32_t *dims;     /* levels x 3: intervals per axis (x, y, z) */
+    const int32_t *axis_map; /* levels x (nx + ny + nz): voxel index -> interval index */
+    const int32_t *ivl_off;  /* levels x 3: offset of the axis' (lo, hi) pairs in ivl */
+    const int32_t *ivl;      /* (lo, hi) voxel bounds of every interval, n_ivl ints */
+    const int64_t *box_off;  /* levels: first box of the level in state / srange */
+    const uint8_t *state;    /* per box, [bz][by][bx] within a level, n_boxes bytes */
+    const double *srange;    /* per box (smin, smax), 2 x n_boxes doubles */
+    int64_t n_ivl, n_boxes;
+} vc_octree_desc;
 
 /* counters written by vc_render (device, VC_NUM_COUNTERS x uint64):
  *   [0] volume samples taken by marching, fine scan, bisection and the
@@ -131,6 +154,8 @@ VC_API int vc_volume_create(int device, const void *h_data, int dtype, int nx, i
 VC_API int vc_volume_create_device(int device, const void *d_data, int dtype, int nx, int ny, int nz,
                             const double spacing[3], vc_volume **out);
 VC_API int vc_volume_destroy(vc_volume *vol);
+/* Attach the octree used by adaptive stepping (octree.py:52-136). */
+VC_API int vc_volume_set_octree(vc_volume *vol, const vc_octree_desc *desc);
 /* device pointer of the voxel array (read-only) */
 VC_API int vc_volume_data(const vc_volume *vol, const void **d_data);
 

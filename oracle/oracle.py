@@ -61,6 +61,12 @@ class _Params(ctypes.Structure):
         ("fine", ctypes.c_double),
         ("refine_iters", ctypes.c_int32),
         ("bg", ctypes.c_double * 4),
+        ("use_adaptive", ctypes.c_int32),
+        ("adapt_jump", ctypes.c_int32),
+        ("detail_eps", ctypes.c_double),
+        ("nbounds", ctypes.POINTER(ctypes.c_int32)),
+        ("sminmax", ctypes.POINTER(ctypes.c_double)),
+        ("nchildren", ctypes.POINTER(ctypes.c_int32)),
     ]
 
 
@@ -329,18 +335,94 @@ def make_params(dims, spacing, spec: dict) -> _Params:
     return P
 
 
+# ---------------------------------------------------------------- octree (adaptive mode)
+
+def build_octree_flat(arr, min_block=4, max_depth=8):
+    """Restatement of octree.build_octree + flat_arrays (octree.py:52-136):
+    returns (nbounds (N,6) int32, sminmax (N,2) float64, nchildren (N,8)
+    int32) in the reference's node order.  Plain recursion; for the small
+    grids the tests use."""
+    a = np.asarray(arr)
+    nz, ny, nx = a.shape
+
+    def ranges(lo, hi):
+        blk = a[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]]
+        pad = a[max(lo[2] - 1, 0):min(hi[2] + 1, nz), max(lo[1] - 1, 0):min(hi[1] + 1, ny),
+                max(lo[0] - 1, 0):min(hi[0] + 1, nx)]
+        return int(blk.min()), int(blk.max()), int(pad.min()), int(pad.max())
+
+    def make(lo, hi, depth):
+        vmin, vmax, smin, smax = ranges(lo, hi)
+        return {"lo": lo, "hi": hi, "vmin": vmin, "vmax": vmax, "smin": smin, "smax": smax,
+                "depth": depth, "children": []}
+
+    root = make((0, 0, 0), (nx, ny, nz), 0)
+    stack = [root]
+    while stack:
+        node = stack.pop()
+        ext = tuple(h - l for l, h in zip(node["lo"], node["hi"]))
+        if node["vmin"] == node["vmax"] or max(ext) <= min_block or node["depth"] >= max_depth:
+            continue
+        cuts = []
+        for ax in range(3):
+            if ext[ax] >= 2:
+                cuts.append([(node["lo"][ax], node["lo"][ax] + ext[ax] // 2),
+                             (node["lo"][ax] + ext[ax] // 2, node["hi"][ax])])
+            else:
+                cuts.append([(node["lo"][ax], node["hi"][ax])])
+        for zc in cuts[2]:
+            for yc in cuts[1]:
+                for xc in cuts[0]:
+                    ch = make((xc[0], yc[0], zc[0]), (xc[1], yc[1], zc[1]), node["depth"] + 1)
+                    node["children"].append(ch)
+                    stack.append(ch)
+    nodes = []
+    stack = [root]
+    while stack:
+        n = stack.pop()
+        nodes.append(n)
+        stack.extend(n["children"])
+    index = {id(n): i for i, n in enumerate(nodes)}
+    nb = np.empty((len(nodes), 6), np.int32)
+    sm = np.empty((len(nodes), 2), np.float64)
+    ch = np.full((len(nodes), 8), -1, np.int32)
+    for i, n in enumerate(nodes):
+        nb[i, :3] = n["lo"]
+        nb[i, 3:] = n["hi"]
+        sm[i] = (n["smin"], n["smax"])
+        for c, kid in enumerate(n["children"]):
+            ch[i, c] = index[id(kid)]
+    return nb, sm, ch
+
+
 def render(arr, spacing, spec: dict, threads=None, rows=None):
-    """Brute-force frame (render_frame(..., use_octree=False)).
+    """Brute-force frame (render_frame(..., use_octree=False)); with
+    settings.use_adaptive the reference's adaptive stride over its octree.
 
     Returns (pixels (H,W,4) uint8, sample_count).  `rows` = (y0, y1)
     restricts the work to a row range (other rows stay zero)."""
     arr, code, nx, ny, nz = _vol(arr)
     P = make_params((nx, ny, nz), spacing, spec)
+    s = spec.get("settings", {})
+    keep = None
+    if s.get("use_adaptive"):
+        nb, sm, ch = build_octree_flat(arr, s.get("octree_min_block", 4), s.get("octree_max_depth", 8))
+        keep = (nb, sm, ch)
+        P.use_adaptive = 1
+        P.adapt_jump = int(s.get("adaptive_factor", 4))
+        eps = s.get("detail_epsilon")
+        if eps is None:
+            eps = 0.01 * max(1, int(arr.max()) - int(arr.min()))
+        P.detail_eps = float(eps)
+        P.nbounds = nb.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        P.sminmax = sm.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        P.nchildren = ch.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
     out = np.zeros((P.height, P.width, 4), np.uint8)
     y0, y1 = rows if rows is not None else (0, P.height)
     count = lib().vco_render(arr.ctypes.data, code, nx, ny, nz, ctypes.byref(P), int(y0),
                              int(y1), out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
                              int(threads or os.cpu_count() or 1))
+    del keep
     return out, int(count)
 
 

@@ -10,10 +10,12 @@
  * reference kernel layer /root/reference/pkg/src/voxelcast/_kernels.py
  * (numba, fastmath off, no FMA contraction -- compile with
  * -ffp-contract=off).  Every function cites the reference lines it
- * follows.  The octree / adaptive-step paths are not restated: the oracle
+ * follows.  The octree's empty-space segments are not restated: the oracle
  * is the brute-force renderer (render_frame(..., use_octree=False)), which
  * the reference guarantees is pixel-identical to the octree path
- * (pkg/tests/test_render.py:125-139).
+ * (pkg/tests/test_render.py:125-139).  The adaptive stride
+ * (use_adaptive, _kernels.py:437-463) is restated over the reference's flat
+ * octree arrays (built by oracle.build_octree_flat).
  *
  * Parity is pinned against golden fixtures produced by running the
  * reference itself (tests/golden/make_golden.py).
@@ -61,6 +63,13 @@ typedef struct {
     double coarse, fine;
     int32_t refine_iters;
     double bg[4];
+    /* adaptive stride (use_adaptive, _kernels.py:437-463) over the
+     * reference's flat octree arrays (octree.py:111-136) */
+    int32_t use_adaptive, adapt_jump;
+    double detail_eps;
+    const int32_t *nbounds;   /* N x 6 (lo xyz, hi xyz) */
+    const double *sminmax;    /* N x 2 padded range */
+    const int32_t *nchildren; /* N x 8, -1 padded */
 } vco_params;
 
 /* _kernels.py:35-37 */
@@ -254,12 +263,86 @@ static inline void voxel_pos(const double org[3], const double dirv[3], const do
     p[2] = (org[2] + t * dirv[2]) / sp[2] - 0.5;
 }
 
-/* _kernels.py:367-465, single segment [t_enter, t_exit], no octree, no
- * adaptive stride (the use_octree=False / use_adaptive=False branch). */
-static int first_hit(const vco_vol *v, const double sp[3], const double org[3],
-                     const double dirv[3], double t_enter, double t_exit, double coarse,
-                     double fine, double t_low, double t_high, int interp, int64_t *counter,
-                     double *t_hit, double *t_before, int *bracket) {
+/* _kernels.py:345-364 */
+static int leaf_for_point(const vco_params *P, int ix, int iy, int iz) {
+    int idx = 0;
+    while (P->nchildren[idx * 8] >= 0) {
+        int nxt = idx;
+        for (int c = 0; c < 8; c++) {
+            int ci = P->nchildren[idx * 8 + c];
+            if (ci < 0) break;
+            const int32_t *b = P->nbounds + ci * 6;
+            if (b[0] <= ix && ix < b[3] && b[1] <= iy && iy < b[4] && b[2] <= iz && iz < b[5]) {
+                nxt = ci;
+                break;
+            }
+        }
+        if (nxt == idx) break;
+        idx = nxt;
+    }
+    return idx;
+}
+
+/* _kernels.py:227-264 */
+static int node_interval(const vco_params *P, int idx, const double sp[3], const double org[3],
+                         const double dirv[3], double *t0, double *t1) {
+    const int32_t *b = P->nbounds + idx * 6;
+    double tmin = -1e300, tmax = 1e300;
+    for (int a = 0; a < 3; a++) {
+        double lo = (double)b[a] * sp[a], hi = (double)b[3 + a] * sp[a];
+        double o = org[a], d = dirv[a];
+        if (d == 0.0) {
+            if (o < lo || o > hi) return 0;
+        } else {
+            double inv = 1.0 / d;
+            double ta = (lo - o) * inv, tb = (hi - o) * inv;
+            if (ta > tb) {
+                double s = ta;
+                ta = tb;
+                tb = s;
+            }
+            if (ta > tmin) tmin = ta;
+            if (tb < tmax) tmax = tb;
+        }
+    }
+    if (tmin > tmax) return 0;
+    *t0 = tmin;
+    *t1 = tmax;
+    return 1;
+}
+
+/* _kernels.py:437-463: lattice steps after an out-of-window sample at p */
+static int64_t adaptive_stride(const vco_vol *v, const vco_params *P, const double sp[3],
+                               const double org[3], const double dirv[3], const double p[3],
+                               int64_t k, double t_enter, double coarse) {
+    int64_t step_k = 1;
+    int ix = (int)floor(p[0]), iy = (int)floor(p[1]), iz = (int)floor(p[2]);
+    if (ix < 0) ix = 0;
+    if (iy < 0) iy = 0;
+    if (iz < 0) iz = 0;
+    if (ix > v->nx - 1) ix = v->nx - 1;
+    if (iy > v->ny - 1) iy = v->ny - 1;
+    if (iz > v->nz - 1) iz = v->nz - 1;
+    int leaf = leaf_for_point(P, ix, iy, iz);
+    if (P->sminmax[leaf * 2 + 1] - P->sminmax[leaf * 2] < P->detail_eps) {
+        double la, lb;
+        if (node_interval(P, leaf, sp, org, dirv, &la, &lb)) {
+            step_k = P->adapt_jump;
+            int64_t kex = (int64_t)floor((lb - t_enter) / coarse) + 1;
+            if (kex - k < step_k) step_k = kex - k;
+            if (step_k < 1) step_k = 1;
+        }
+    }
+    return step_k;
+}
+
+/* _kernels.py:367-465, single segment [t_enter, t_exit], no octree
+ * segments (the use_octree=False branch); adaptive stride when P (non-NULL)
+ * asks for it. */
+static int first_hit_p(const vco_vol *v, const vco_params *P, const double sp[3], const double org[3],
+                       const double dirv[3], double t_enter, double t_exit, double coarse,
+                       double fine, double t_low, double t_high, int interp, int64_t *counter,
+                       double *t_hit, double *t_before, int *bracket) {
     int64_t k = 0;
     double s0 = t_enter, s1 = t_exit;
     if (s1 > t_exit) s1 = t_exit;
@@ -296,11 +379,20 @@ static int first_hit(const vco_vol *v, const double sp[3], const double org[3],
                 j += 1;
             }
         }
-        k += 1;
+        if (P && P->use_adaptive) k += adaptive_stride(v, P, sp, org, dirv, p, k, t_enter, coarse);
+        else k += 1;
     }
     *t_hit = *t_before = 0.0;
     *bracket = 0;
     return 0;
+}
+
+static int first_hit(const vco_vol *v, const double sp[3], const double org[3],
+                     const double dirv[3], double t_enter, double t_exit, double coarse,
+                     double fine, double t_low, double t_high, int interp, int64_t *counter,
+                     double *t_hit, double *t_before, int *bracket) {
+    return first_hit_p(v, NULL, sp, org, dirv, t_enter, t_exit, coarse, fine, t_low, t_high, interp,
+                       counter, t_hit, t_before, bracket);
 }
 
 /* _kernels.py:468-487 */
@@ -407,9 +499,9 @@ static void render_rows(const vco_vol *v, const vco_params *P, int y0, int y1, u
             double t_enter = iv[0], t_exit = iv[1];
             double t_in, t_before;
             int bracket;
-            int found = first_hit(v, P->spacing, org, dirv, t_enter, t_exit, P->coarse, P->fine,
-                                  P->t_low, P->t_high, P->interp, counter, &t_in, &t_before,
-                                  &bracket);
+            int found = first_hit_p(v, P, P->spacing, org, dirv, t_enter, t_exit, P->coarse, P->fine,
+                                    P->t_low, P->t_high, P->interp, counter, &t_in, &t_before,
+                                    &bracket);
             if (!found) {
                 o[0] = bgr; o[1] = bgg; o[2] = bgb; o[3] = bga;
                 continue;

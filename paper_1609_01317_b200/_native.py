@@ -34,6 +34,7 @@ DTYPE_CODES = {np.dtype(np.uint8): VC_U8, np.dtype(np.uint16): VC_U16, np.dtype(
 EXPORTS = (
     "vc_abi_version", "vc_render_params_size", "vc_last_error", "vc_device_count",
     "vc_volume_create", "vc_volume_create_device", "vc_volume_destroy", "vc_volume_data",
+    "vc_volume_set_octree",
     "vc_gradient_prepass", "vc_gradient_volume", "vc_gradient_prepass_into",
     "vc_render", "vc_render_profiled", "vc_render_host",
     "vc_sample_points", "vc_gradient_points",
@@ -63,6 +64,21 @@ class RenderParams(ctypes.Structure):
         ("coarse", ctypes.c_double), ("fine", ctypes.c_double),
         ("bg", ctypes.c_double * 4),
         ("skip_empty", ctypes.c_int32), ("grad_source", ctypes.c_int32),
+        ("use_adaptive", ctypes.c_int32), ("adapt_jump", ctypes.c_int32),
+        ("detail_eps", ctypes.c_double),
+    ]
+
+
+class OctreeDesc(ctypes.Structure):
+    """Mirror of vc_octree_desc."""
+
+    _fields_ = [
+        ("levels", ctypes.c_int32),
+        ("dims", ctypes.POINTER(ctypes.c_int32)), ("axis_map", ctypes.POINTER(ctypes.c_int32)),
+        ("ivl_off", ctypes.POINTER(ctypes.c_int32)), ("ivl", ctypes.POINTER(ctypes.c_int32)),
+        ("box_off", ctypes.POINTER(ctypes.c_int64)), ("state", ctypes.POINTER(ctypes.c_uint8)),
+        ("srange", ctypes.POINTER(ctypes.c_double)),
+        ("n_ivl", ctypes.c_int64), ("n_boxes", ctypes.c_int64),
     ]
 
 
@@ -104,6 +120,7 @@ def load(build_if_missing: bool = True):
                                          ctypes.c_int, dp, ctypes.POINTER(vp)], ctypes.c_int),
             "vc_volume_destroy": ([vp], ctypes.c_int),
             "vc_volume_data": ([vp, ctypes.POINTER(vp)], ctypes.c_int),
+            "vc_volume_set_octree": ([vp, ctypes.POINTER(OctreeDesc)], ctypes.c_int),
             "vc_gradient_prepass": ([vp, ctypes.c_int, vp], ctypes.c_int),
             "vc_gradient_volume": ([vp, ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
             "vc_gradient_prepass_into": ([vp, ctypes.c_int, vp, vp], ctypes.c_int),

@@ -45,6 +45,7 @@ struct vc_volume {
     double vmin = 0.0, vmax = 0.0;  // value range (from the macrocell grid)
     float4* d_grad[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t grad_ready[3] = {nullptr, nullptr, nullptr};
+    vc::OctDev oct{};  // device octree for adaptive stepping (owned buffers)
     uint8_t* d_scratch = nullptr;
     size_t scratch_bytes = 0;
     uint64_t* d_counters = nullptr;
@@ -152,6 +153,17 @@ int finish_create(vc_volume* v) {
     return VC_OK;
 }
 
+void free_octree(vc_volume* v) {
+    cudaFree((void*)v->oct.dims);
+    cudaFree((void*)v->oct.amap);
+    cudaFree((void*)v->oct.ivl_off);
+    cudaFree((void*)v->oct.ivl);
+    cudaFree((void*)v->oct.box_off);
+    cudaFree((void*)v->oct.state);
+    cudaFree((void*)v->oct.srange);
+    v->oct = vc::OctDev{};
+}
+
 void release(vc_volume* v) {
     if (!v) return;
     DeviceGuard g(v->device);
@@ -165,6 +177,7 @@ void release(vc_volume* v) {
     }
     for (auto& e : v->grad_ready)
         if (e) cudaEventDestroy(e);
+    free_octree(v);
     for (auto& p : v->d_grad) cudaFree(p);
     cudaFree(v->d_scratch);
     cudaFree(v->d_counters);
@@ -286,6 +299,7 @@ int validate_params(const vc_render_params* p, int* local_rows) {
     if (!(p->coarse > 0.0) || !(p->fine > 0.0)) return fail(VC_ERR_INVALID, "steps must be positive");
     if (p->refine_iters < 0) return fail(VC_ERR_INVALID, "refine_iters must be >= 0");
     if (!(p->mu_water > 0.0)) return fail(VC_ERR_INVALID, "mu_water must be positive");
+    if (p->use_adaptive && p->adapt_jump < 1) return fail(VC_ERR_INVALID, "adaptive_factor must be >= 1");
     if (p->grad_source != VC_GRAD_TAPS && p->grad_source != VC_GRAD_VOLUME)
         return fail(VC_ERR_INVALID, "grad_source must be VC_GRAD_TAPS or VC_GRAD_VOLUME");
     const long long nb = (p->height + p->band_rows - 1) / p->band_rows;
@@ -311,6 +325,7 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
     L.amax = std::max(std::fabs(v->vmin), std::fabs(v->vmax));
     if (!std::isfinite(L.amax)) L.amax = -1.0;  // no float32 pre-test
     L.rp = make_raypos(v);
+    L.oct = v->oct;
     L.out = d_rgba;
     L.local_rows = local_rows;
     L.counters = d_counters;
@@ -333,7 +348,10 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
     L.my = v->my;
     L.occ = nullptr;
     const bool zero_in_window = p->t_low <= 0.0 && 0.0 <= p->t_high;
-    L.skip_on = (p->skip_empty && !zero_in_window) ? 1 : 0;
+    // adaptive strides depend on the exact lattice sequence: no skipping
+    L.skip_on = (p->skip_empty && !zero_in_window && !p->use_adaptive) ? 1 : 0;
+    if (p->use_adaptive && v->oct.levels == 0)
+        return fail(VC_ERR_INVALID, "use_adaptive needs an octree (vc_volume_set_octree)");
     vc_volume::WindowField* field = nullptr;
     if (L.skip_on) {
         int rc = window_field(v, p->t_low, p->t_high, s, &field);
@@ -382,6 +400,42 @@ int vc_volume_create_device(int device, const void* d_data, int dtype, int nx, i
 
 int vc_volume_destroy(vc_volume* vol) {
     release(vol);
+    return VC_OK;
+}
+
+int vc_volume_set_octree(vc_volume* vol, const vc_octree_desc* d) {
+    if (!vol || !d) return fail(VC_ERR_INVALID, "null argument");
+    if (d->levels < 1 || d->levels > 17) return fail(VC_ERR_INVALID, "octree levels must be in [1, 17]");
+    if (!d->dims || !d->axis_map || !d->ivl_off || !d->ivl || !d->box_off || !d->state || !d->srange ||
+        d->n_ivl <= 0 || d->n_boxes <= 0)
+        return fail(VC_ERR_INVALID, "incomplete octree description");
+    DeviceGuard g(vol->device);
+    std::lock_guard<std::mutex> lk(vol->mu);
+    VC_CUDA(cudaDeviceSynchronize());  // renders in flight may read the old tree
+    free_octree(vol);
+    const size_t L = (size_t)d->levels, nmap = L * (size_t)(vol->nx + vol->ny + vol->nz);
+    auto up = [](const void* src, size_t bytes, const void** dst) -> cudaError_t {
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) return e;
+        *dst = p;
+        return cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice);
+    };
+    vc::OctDev o{};
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = up(d->dims, L * 3 * sizeof(int32_t), (const void**)&o.dims);
+    if (e == cudaSuccess) e = up(d->axis_map, nmap * sizeof(int32_t), (const void**)&o.amap);
+    if (e == cudaSuccess) e = up(d->ivl_off, L * 3 * sizeof(int32_t), (const void**)&o.ivl_off);
+    if (e == cudaSuccess) e = up(d->ivl, (size_t)d->n_ivl * sizeof(int32_t), (const void**)&o.ivl);
+    if (e == cudaSuccess) e = up(d->box_off, L * sizeof(int64_t), (const void**)&o.box_off);
+    if (e == cudaSuccess) e = up(d->state, (size_t)d->n_boxes, (const void**)&o.state);
+    if (e == cudaSuccess) e = up(d->srange, (size_t)d->n_boxes * 2 * sizeof(double), (const void**)&o.srange);
+    vol->oct = o;
+    if (e != cudaSuccess) {
+        free_octree(vol);
+        return cuda_fail(e, "octree upload");
+    }
+    vol->oct.levels = d->levels;
     return VC_OK;
 }
 

@@ -319,11 +319,72 @@ __device__ __forceinline__ bool start_ray(Ctx<T>& C, const vc_render_params& P, 
     return true;
 }
 
+// Adaptive stride after an out-of-window first-hit sample at p with lattice
+// index k (_kernels.py:437-463): leaf_for_point (:345-364) over the level
+// grid, then _node_interval (:227-264) of the leaf when its padded range is
+// below detail_eps.  Same float64 operations as the reference.
+template <typename T>
+__device__ __forceinline__ double adaptive_stride(const OctDev& o, const Ctx<T>& C, const vc_render_params& P,
+                                                  const double p[3], double k, double t_enter) {
+    const int n3[3] = {C.v.nx, C.v.ny, C.v.nz};
+    int ic[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        double r;
+        int i = floor_pos(p[a], r);
+        i = i < 0 ? 0 : (i > n3[a] - 1 ? n3[a] - 1 : i);
+        ic[a] = i;
+    }
+    const int stride_map = C.v.nx + C.v.ny + C.v.nz;
+    int L = 0, b[3] = {0, 0, 0};
+    long long leaf = 0;
+    for (L = 0; L < o.levels; L++) {
+        const int* m = o.amap + (size_t)L * stride_map;
+        b[0] = __ldg(m + ic[0]);
+        b[1] = __ldg(m + C.v.nx + ic[1]);
+        b[2] = __ldg(m + C.v.nx + C.v.ny + ic[2]);
+        leaf = __ldg(o.box_off + L) +
+               ((long long)b[2] * __ldg(o.dims + 3 * L + 1) + b[1]) * __ldg(o.dims + 3 * L + 0) + b[0];
+        if (__ldg(o.state + leaf) == 2) break;
+    }
+    if (L == o.levels) return 1.0;  // unreachable for a well-formed tree
+    const double smin = __ldg(o.srange + 2 * leaf), smax = __ldg(o.srange + 2 * leaf + 1);
+    if (!(dsub(smax, smin) < P.detail_eps)) return 1.0;
+    // _node_interval of the leaf box
+    double tmin = -1e300, tmax = 1e300;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        const int* iv = o.ivl + __ldg(o.ivl_off + 3 * L + a) + 2 * b[a];
+        const double lo = dmul((double)__ldg(iv), C.rp.s[a]);
+        const double hi = dmul((double)__ldg(iv + 1), C.rp.s[a]);
+        const double ov = C.rp.o[a], d = C.rp.d[a];
+        if (d == 0.0) {
+            if (ov < lo || ov > hi) return 1.0;
+        } else {
+            const double inv = ddiv(1.0, d);
+            double ta = dmul(dsub(lo, ov), inv), tb = dmul(dsub(hi, ov), inv);
+            if (ta > tb) {
+                const double sw = ta;
+                ta = tb;
+                tb = sw;
+            }
+            if (ta > tmin) tmin = ta;
+            if (tb < tmax) tmax = tb;
+        }
+    }
+    if (tmin > tmax) return 1.0;
+    double step = (double)P.adapt_jump;
+    const double kex = floor(ddiv(dsub(tmax, t_enter), P.coarse)) + 1.0;
+    if (dsub(kex, k) < step) step = dsub(kex, k);
+    if (step < 1.0) step = 1.0;
+    return step;
+}
+
 // One lattice step of the march base + k*coarse (first_hit's loop body,
 // _kernels.py:410-436 / the composite loop :756-765).
 template <typename T, int INTERP>
 __device__ __forceinline__ void march_step(const Ctx<T>& C, const vc_render_params& P, RayState& R,
-                                           unsigned& nsamp, unsigned& nskip) {
+                                           unsigned& nsamp, unsigned& nskip, const OctDev* oct = nullptr) {
     const double t = dadd(R.base, dmul(R.k, P.coarse));
     if (t > R.lim) {
         R.exhausted = true;
@@ -334,6 +395,10 @@ __device__ __forceinline__ void march_step(const Ctx<T>& C, const vc_render_para
     const int w = march_sample<T, INTERP>(C, P, p, t, R.k, R.base, nskip);
     if (w < 0) return;
     nsamp++;
+    if (oct != nullptr && !w) {  // first-hit stage, adaptive mode
+        R.k += adaptive_stride(*oct, C, P, p, R.k, R.t_enter);
+        return;
+    }
     R.k += 1.0;
     if (w) {
         R.found = true;
@@ -507,7 +572,8 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
                                                           RayPos rp0, const uint8_t* __restrict__ dist, int mx,
                                                           int my, int skip_on, uchar4* __restrict__ out,
                                                           int local_rows, unsigned long long* counters,
-                                                          FrameWork* work, HitEntry* __restrict__ hits) {
+                                                          FrameWork* work, HitEntry* __restrict__ hits,
+                                                          OctDev oct) {
     const unsigned FULL = 0xffffffffu;
     const int tiles_x = (P.width + 7) >> 3;
     const unsigned total = (unsigned)tiles_x * (unsigned)((local_rows + 3) >> 2) * 32u;
@@ -547,7 +613,7 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
             if (mneed == 0) break;
             const unsigned mact = __ballot_sync(FULL, active);
             if (__popc(mact & ~mneed) * READY_DEN >= __popc(mact) * VC_FH_READY) break;
-            if (need) march_step<T, INTERP>(C, P, R, nsamp, nskip);
+            if (need) march_step<T, INTERP>(C, P, R, nsamp, nskip, P.use_adaptive ? &oct : nullptr);
         }
         const bool hit = active && R.found;
         double t_star = 0.0;
@@ -693,7 +759,8 @@ static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
     firsthit_kernel<T, OP, INTERP><<<persistent_blocks(firsthit_kernel<T, OP, INTERP>, (tiles + 3) / 4), 128, 0,
                                      stream>>>(*L.p, vol, L.rp, L.occ, L.mx, L.my, L.skip_on,
                                                reinterpret_cast<uchar4*>(L.out), L.local_rows,
-                                               reinterpret_cast<unsigned long long*>(L.counters), fw, hits);
+                                               reinterpret_cast<unsigned long long*>(L.counters), fw, hits,
+                                               L.oct);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (L.ev[1]) cudaEventRecord(L.ev[1], stream);

@@ -16,6 +16,18 @@ namespace vc {
 constexpr int MC_SHIFT = VC_MC_SHIFT;
 constexpr int MC_EDGE = 1 << MC_SHIFT;
 
+// device copy of the level-grid octree (vc_octree_desc); levels == 0: none
+struct OctDev {
+    int levels;
+    const int* dims;
+    const int* amap;
+    const int* ivl_off;
+    const int* ivl;
+    const long long* box_off;
+    const uint8_t* state;
+    const double* srange;
+};
+
 struct RenderLaunch {
     const vc_render_params* p;
     int dtype;
@@ -33,6 +45,7 @@ struct RenderLaunch {
     void* work;           // frame work counters (FrameWork, zeroed per launch)
     void* hits;           // first-hit queue, >= local_rows * width entries
     cudaEvent_t ev[3];    // optional: recorded before stage 1, between, after stage 2
+    OctDev oct;           // adaptive stepping (levels == 0 when unused)
 };
 
 cudaError_t launch_raycast(const RenderLaunch& L, cudaStream_t s);

@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native
-from .raycast import FrameBuffer, RenderSettings, Scene, render_params, sample_count_of
+from .raycast import FrameBuffer, RenderSettings, Scene, prepare_device, render_params, sample_count_of
 from .volume import Volume, device_volume
 
 
@@ -90,7 +90,7 @@ def render_frame_distributed(volume: Volume, scene: Scene, settings: RenderSetti
     rank = dist.get_rank(group)
     dev = torch.cuda.current_device()
     plan = BandPlan(settings.height, settings.width, band_rows, world, rank)
-    dv = device_volume(volume, dev)
+    dv = prepare_device(volume, settings, dev)
     P = render_params(volume, scene, settings, band_rows=band_rows, band_first=rank, band_step=world)
     local = torch.empty((max(plan.local_rows, 1), settings.width, 4), dtype=torch.uint8, device=dev)
     cnt = torch.zeros(_native.NUM_COUNTERS, dtype=torch.int64, device=dev)

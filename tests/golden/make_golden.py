@@ -64,7 +64,11 @@ def ref_settings(spec):
         kw["interpolation"] = vc.InterpolationMode(s["interpolation"])
     if "background" in s:
         kw["background"] = tuple(s["background"])
-    return vc.RenderSettings(use_octree=False, **kw)
+    for key in ("use_adaptive", "adaptive_factor", "detail_epsilon", "octree_min_block",
+                "octree_max_depth"):
+        if key in s:
+            kw[key] = s[key]
+    return vc.RenderSettings(use_octree=bool(s.get("use_octree", False)), **kw)
 
 
 def render_ref(arr, spacing, spec):
@@ -204,6 +208,23 @@ def frame_cases():
                         camera={"azimuth": 45.0},
                         settings={"width": 40, "height": 40, "operator": "sobel3d",
                                   "mode": "composited"})))
+    # adaptive stride (use_adaptive, _kernels.py:437-463) -- test_render.py:142-152 scene
+    sph8 = vc.make_phantom("sphere", 64, radius=8).as_array().copy()
+    d64 = default_spec((64, 64, 64))
+    for oct_on in (False, True):
+        cases.append((f"adaptive_sphere64_octree{int(oct_on)}", sph8, (1.0, 1.0, 1.0),
+                      with_(d64, settings={"width": 64, "height": 64, "use_adaptive": True,
+                                           "adaptive_factor": 4, "use_octree": oct_on})))
+        cases.append((f"adaptive_ct48_zh_composited_octree{int(oct_on)}", ct, (1.0, 1.0, 1.0),
+                      with_(d48, camera={"azimuth": 20.0, "elevation": 10.0},
+                            settings={"width": 64, "height": 48, "operator": "zucker-hummel",
+                                      "mode": "composited", "use_adaptive": True,
+                                      "adaptive_factor": 3, "use_octree": oct_on})))
+    cases.append(("adaptive_noise16_detail", noise16, (1.0, 1.0, 1.0),
+                  with_(d16, window=[3000.0, 4095.0], camera={"azimuth": 30.0},
+                        settings={"width": 40, "height": 32, "operator": "sobel3d",
+                                  "use_adaptive": True, "adaptive_factor": 3,
+                                  "detail_epsilon": 3500.0, "octree_min_block": 2})))
     empty = np.zeros((16, 16, 16), np.uint16)
     cases.append(("empty16", empty, (1.0, 1.0, 1.0),
                   with_(d16, settings={"width": 24, "height": 24,

@@ -40,6 +40,10 @@ def product_settings(spec: dict, **over) -> vc.RenderSettings:
         kw["interpolation"] = vc.InterpolationMode(s["interpolation"])
     if "background" in s:
         kw["background"] = tuple(s["background"])
+    for key in ("use_adaptive", "adaptive_factor", "detail_epsilon", "octree_min_block",
+                "octree_max_depth", "use_octree"):
+        if key in s:
+            kw[key] = s[key]
     kw.update(over)
     return vc.RenderSettings(**kw)
 
@@ -60,5 +64,8 @@ def spec_of(scene_settings) -> dict:
         "settings": {"width": st.width, "height": st.height, "operator": st.operator.value,
                      "interpolation": st.interpolation.value, "mode": st.mode,
                      "coarse_step": st.coarse_step, "fine_step": st.fine_step,
-                     "refine_iters": st.refine_iters, "background": list(st.background)},
+                     "refine_iters": st.refine_iters, "background": list(st.background),
+                     "use_adaptive": st.use_adaptive, "adaptive_factor": st.adaptive_factor,
+                     "detail_epsilon": st.detail_epsilon, "octree_min_block": st.octree_min_block,
+                     "octree_max_depth": st.octree_max_depth},
     }
