@@ -304,3 +304,23 @@ def test_adaptive_stride_vs_oracle(mode):
         assert fb.sample_count == want_count
         fb2 = vc.render_frame(vol, sc, replace(st2, gradient_source="volume"))
         assert maxdiff(fb2.pixels, want) <= 1
+
+
+@pytest.mark.parametrize("shape", [(1, 8, 8), (8, 1, 8), (2, 2, 2), (3, 17, 5), (1, 1, 1)])
+@pytest.mark.parametrize("mode", ["surface", "composited"])
+def test_degenerate_grids_vs_oracle(shape, mode):
+    """Cell clamping for n = 1 / 2 (_kernels.py:52-64) and thin slabs."""
+    rng = np.random.default_rng(sum(shape))
+    arr = rng.integers(0, 4096, size=shape, dtype=np.uint16)
+    vol = vc.Volume.from_array(arr)
+    for op in vc.OperatorKind:
+        sc = vc.default_scene(vol)
+        sc = vc.Scene(camera=vc.Camera(eye=sc.camera.eye, target=sc.camera.target, azimuth=23.0,
+                                       elevation=11.0), light=sc.light,
+                      window=vc.ThresholdWindow(1200.0, 4095.0))
+        st = vc.RenderSettings(width=24, height=20, operator=op, mode=mode, use_octree=False)
+        want, cnt = oracle.render(arr, vol.spacing, spec_of((sc, st)))
+        fb = vc.render_frame(vol, sc, st)
+        assert np.array_equal(fb.pixels, want) and fb.sample_count == cnt, (shape, op)
+        fb = vc.render_frame(vol, sc, product_settings_from(st, use_octree=True, gradient_source="volume"))
+        assert maxdiff(fb.pixels, want) <= 1
