@@ -58,6 +58,8 @@ def parse():
                     help="target CPU time of the bounded cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gather", default="peer", choices=("peer", "nccl"),
+                    help="N>1: fused NVLink peer stores (validated) or NCCL all-gather")
     return ap.parse_args()
 
 
@@ -271,15 +273,47 @@ def run_ours(args):
     sp = ctypes.c_void_p(stream.cuda_stream)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{dev}")
 
-    from paper_1609_01317_b200.dispatch import BandPlan, TileGather
+    from paper_1609_01317_b200.dispatch import BandPlan, PeerFrames, TileGather
 
     plan = BandPlan(H, W, band_rows=8, world=world, rank=rank)
     local_buf = torch.empty((max(plan.local_rows, 1), W, 4), dtype=torch.uint8, device=f"cuda:{dev}")
-    gather = TileGather(plan, device=f"cuda:{dev}") if world > 1 else None
+    gather_mode = "none"
+    gather = peers = None
+    if world > 1:
+        gather = TileGather(plan, device=f"cuda:{dev}")
+        gather_mode = "nccl"
+        if args.gather == "peer":
+            # fused path: the raycast kernels store pixels into every rank's
+            # frame over NVLink (two frame buffers, alternating); validated
+            # against the NCCL path on one frame before use
+            try:
+                peers = [PeerFrames(H, W, dev), PeerFrames(H, W, dev)]
+                sc, st = frame(0)
+                P = render_params(vol, sc, st, band_rows=plan.band_rows, band_first=rank, band_step=world)
+                peers[0].render(dv, P, 0, stream.cuda_stream)
+                torch.cuda.synchronize(dev)
+                torch.distributed.barrier()
+                got = peers[0].download(np.empty((H, W, 4), np.uint8))
+                _native.check(L.vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(local_buf.data_ptr()),
+                                          None, sp))
+                want = gather(local_buf).cpu().numpy()
+                ok = torch.tensor([int(np.array_equal(got, want))], device=f"cuda:{dev}")
+                torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)
+                if int(ok.item()) == 1:
+                    gather_mode = "peer (fused NVLink stores, validated against NCCL)"
+                else:
+                    gather_mode = "nccl (peer path failed validation)"
+                    peers = None
+            except Exception as exc:  # recorded in the JSON line, not silent
+                gather_mode = f"nccl (peer path unavailable: {type(exc).__name__}: {exc})"
+                peers = None
 
     def render(i, counters=None):
         sc, st = frame(i)
         P = render_params(vol, sc, st, band_rows=plan.band_rows, band_first=rank, band_step=world)
+        if peers is not None:
+            peers[i & 1].render(dv, P, counters.value if counters is not None else 0, stream.cuda_stream)
+            return None
         _native.check(L.vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(local_buf.data_ptr()),
                                   counters, sp))
         if gather is not None:
@@ -419,6 +453,10 @@ def run_ours(args):
                "render_frame_sync_fps": args.steps / t_sync,
                "note": "h2d per step = the scene/camera parameter block (kernel parameters)"}
 
+    if peers is not None:
+        torch.distributed.barrier()  # no rank still stores into a mapping we unmap
+        for pf in peers:
+            pf.close()
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -453,7 +491,7 @@ def run_ours(args):
                    "mode": args.mode, "gradient_source": args.grad,
                    "empty_space_skipping": not args.no_skip,
                    "l2": "flushed between timed frames (256 MiB write, outside the event pair)",
-                   "parallelism": f"image-plane row bands x{world}"},
+                   "parallelism": f"image-plane row bands x{world}", "gather": gather_mode},
         "gsamples_per_s": w_frame * fps / 1e9,
         "work_per_frame": {"W_ray_samples_bruteforce": w_frame, "K_shades": k_frame,
                            "executed": {"samples": float(ce[0]), "shades": float(ce[1]),

@@ -25,6 +25,7 @@
 #ifndef VOXELCAST_B200_H
 #define VOXELCAST_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -174,6 +175,27 @@ VC_API int vc_gradient_prepass_into(const vc_volume *vol, int op, void *d_out, v
  * d_counters may be NULL. */
 VC_API int vc_render(vc_volume *vol, const vc_render_params *p, uint8_t *d_rgba, uint64_t *d_counters,
               void *stream);
+/* Image-tile render fused with the gather (multi-GPU, one process per GPU):
+ * renders the bands of p (band_first / band_step) and stores every finished
+ * pixel straight into each of the n_frames full (height, width, 4) frame
+ * buffers -- this rank's own and the other ranks' buffers mapped over
+ * NVLink with vc_ipc_open -- at its image row.  d_frames is a device array
+ * of n_frames device pointers.  After every rank's call has completed (host
+ * barrier) all frame buffers hold the whole frame; replaces the separate
+ * NCCL all-gather of packed bands. */
+VC_API int vc_render_to_peers(vc_volume *vol, const vc_render_params *p, void *const *d_frames,
+                              int n_frames, uint64_t *d_counters, void *stream);
+/* Frame buffers shared across processes must be whole allocations (an IPC
+ * handle maps the allocation base): allocate them here. */
+VC_API int vc_device_alloc(int device, size_t bytes, void **d_ptr);
+VC_API int vc_device_free(void *d_ptr);
+VC_API int vc_memcpy_to_host(void *h_dst, const void *d_src, size_t bytes, void *stream);
+/* CUDA IPC helpers for vc_render_to_peers: 64-byte handle of a device
+ * allocation, open a peer's handle on `device`, close it. */
+#define VC_IPC_HANDLE_BYTES 64
+VC_API int vc_ipc_handle(const void *d_ptr, void *handle_out);
+VC_API int vc_ipc_open(int device, const void *handle, void **d_ptr);
+VC_API int vc_ipc_close(void *d_ptr);
 /* vc_render plus per-stage device time (synchronous): stage_ms[0] = the
  * first-hit stage (ray generation, march, fine scan, bisection), stage_ms[1]
  * = the shade / composite stage.  For profiling and the roofline report. */

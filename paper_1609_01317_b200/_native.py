@@ -36,7 +36,9 @@ EXPORTS = (
     "vc_volume_create", "vc_volume_create_device", "vc_volume_destroy", "vc_volume_data",
     "vc_volume_set_octree",
     "vc_gradient_prepass", "vc_gradient_volume", "vc_gradient_prepass_into",
-    "vc_render", "vc_render_profiled", "vc_render_host",
+    "vc_render", "vc_render_profiled", "vc_render_host", "vc_render_to_peers",
+    "vc_ipc_handle", "vc_ipc_open", "vc_ipc_close", "vc_device_alloc", "vc_device_free",
+    "vc_memcpy_to_host",
     "vc_sample_points", "vc_gradient_points",
     "vc_box_interval_rays", "vc_first_hit_rays", "vc_bisect_rays",
 )
@@ -127,6 +129,14 @@ def load(build_if_missing: bool = True):
             "vc_render": ([vp, ctypes.POINTER(RenderParams), vp, vp, vp], ctypes.c_int),
             "vc_render_profiled": ([vp, ctypes.POINTER(RenderParams), vp, vp, vp,
                                     ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
+            "vc_render_to_peers": ([vp, ctypes.POINTER(RenderParams), vp, ctypes.c_int, vp, vp],
+                                   ctypes.c_int),
+            "vc_device_alloc": ([ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(vp)], ctypes.c_int),
+            "vc_device_free": ([vp], ctypes.c_int),
+            "vc_memcpy_to_host": ([vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
+            "vc_ipc_handle": ([vp, vp], ctypes.c_int),
+            "vc_ipc_open": ([ctypes.c_int, vp, ctypes.POINTER(vp)], ctypes.c_int),
+            "vc_ipc_close": ([vp], ctypes.c_int),
             "vc_render_host": ([vp, ctypes.POINTER(RenderParams), vp, u64p,
                                 ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
             "vc_sample_points": ([vp, ctypes.c_int, dp, i64, dp], ctypes.c_int),

@@ -312,8 +312,11 @@ int validate_params(const vc_render_params* p, int* local_rows) {
 }
 
 int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64_t* d_counters,
-                cudaStream_t s, int local_rows, cudaEvent_t* stage_events = nullptr) {
+                cudaStream_t s, int local_rows, cudaEvent_t* stage_events = nullptr,
+                void* const* d_peers = nullptr, int npeers = 0) {
     vc::RenderLaunch L{};
+    L.peers = d_peers;
+    L.npeers = npeers;
     if (stage_events)
         for (int i = 0; i < 3; i++) L.ev[i] = stage_events[i];
     L.p = p;
@@ -479,6 +482,62 @@ int vc_render(vc_volume* vol, const vc_render_params* p, uint8_t* d_rgba, uint64
     DeviceGuard g(vol->device);
     std::lock_guard<std::mutex> lk(vol->mu);
     return render_impl(vol, p, d_rgba, d_counters, static_cast<cudaStream_t>(stream), local_rows);
+}
+
+int vc_render_to_peers(vc_volume* vol, const vc_render_params* p, void* const* d_frames, int n_frames,
+                       uint64_t* d_counters, void* stream) {
+    if (!vol || !d_frames || n_frames < 1 || n_frames > 64) return fail(VC_ERR_INVALID, "need 1..64 frame buffers");
+    int local_rows = 0;
+    int rc = validate_params(p, &local_rows);
+    if (rc) return rc;
+    DeviceGuard g(vol->device);
+    std::lock_guard<std::mutex> lk(vol->mu);
+    return render_impl(vol, p, nullptr, d_counters, static_cast<cudaStream_t>(stream), local_rows, nullptr,
+                       d_frames, n_frames);
+}
+
+int vc_device_alloc(int device, size_t bytes, void** d_ptr) {
+    if (!d_ptr || bytes == 0) return fail(VC_ERR_INVALID, "bad allocation request");
+    DeviceGuard g(device);
+    cudaError_t e = cudaMalloc(d_ptr, bytes);
+    if (e != cudaSuccess) return fail(VC_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    return VC_OK;
+}
+
+int vc_device_free(void* d_ptr) {
+    cudaFree(d_ptr);
+    return VC_OK;
+}
+
+int vc_memcpy_to_host(void* h_dst, const void* d_src, size_t bytes, void* stream) {
+    if (!h_dst || !d_src) return fail(VC_ERR_INVALID, "null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    VC_CUDA(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, s));
+    VC_CUDA(cudaStreamSynchronize(s));
+    return VC_OK;
+}
+
+int vc_ipc_handle(const void* d_ptr, void* handle_out) {
+    if (!d_ptr || !handle_out) return fail(VC_ERR_INVALID, "null argument");
+    cudaIpcMemHandle_t h;
+    VC_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+    memcpy(handle_out, &h, sizeof(h));
+    return VC_OK;
+}
+
+int vc_ipc_open(int device, const void* handle, void** d_ptr) {
+    if (!handle || !d_ptr) return fail(VC_ERR_INVALID, "null argument");
+    DeviceGuard g(device);
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    VC_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return VC_OK;
+}
+
+int vc_ipc_close(void* d_ptr) {
+    if (!d_ptr) return fail(VC_ERR_INVALID, "null argument");
+    VC_CUDA(cudaIpcCloseMemHandle(d_ptr));
+    return VC_OK;
 }
 
 int vc_render_profiled(vc_volume* vol, const vc_render_params* p, uint8_t* d_rgba, uint64_t* d_counters,

@@ -488,6 +488,28 @@ __device__ __forceinline__ bool shade_and_composite(const Ctx<T>& C, const vc_re
 #endif
 constexpr int READY_DEN = 4;
 
+// Where finished pixels go: the packed local rows of this rank (npeers == 0)
+// or, fused with the image-tile gather, every rank's full frame buffer over
+// NVLink peer mappings (npeers > 0): each pixel is stored once per
+// destination straight from the kernel that finished it, so the frame is
+// assembled on all GPUs when the kernels and a host barrier complete -- no
+// separate all-gather pass.
+struct PixelSink {
+    uchar4* out;
+    uchar4* const* peers;
+    int npeers;
+};
+
+__device__ __forceinline__ void put_pixel(const PixelSink& s, const vc_render_params& P, int lr, int px,
+                                          uchar4 o) {
+    if (s.npeers == 0) {
+        s.out[(size_t)lr * P.width + px] = o;
+        return;
+    }
+    const size_t idx = (size_t)image_row(P, lr) * P.width + px;
+    for (int r = 0; r < s.npeers; r++) s.peers[r][idx] = o;
+}
+
 struct HitEntry {  // first-hit queue: pixel, ray and refined parameter t_star
     double t_star, lim;
     double d[3];      // ray direction (bit-exact, saves regenerating the ray)
@@ -570,7 +592,7 @@ __device__ __forceinline__ unsigned warp_ticket(unsigned* ctr, bool want) {
 template <typename T, int OP, int INTERP>
 __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
                                                           RayPos rp0, const uint8_t* __restrict__ dist, int mx,
-                                                          int my, int skip_on, uchar4* __restrict__ out,
+                                                          int my, int skip_on, PixelSink sink,
                                                           int local_rows, unsigned long long* counters,
                                                           FrameWork* work, HitEntry* __restrict__ hits,
                                                           OctDev oct) {
@@ -600,7 +622,7 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
                             active = true;
                             nhit++;
                         } else {
-                            out[(size_t)lr * P.width + px] = bg_pixel(P);
+                            put_pixel(sink, P, lr, px, bg_pixel(P));
                         }
                     }
                 }
@@ -635,7 +657,7 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
             hits[q] = e;
         }
         if (active && (R.found || R.exhausted)) {
-            if (R.exhausted) out[(size_t)lr * P.width + px] = bg_pixel(P);
+            if (R.exhausted) put_pixel(sink, P, lr, px, bg_pixel(P));
             active = false;
         }
     }
@@ -651,7 +673,7 @@ template <typename T, int OP, int INTERP>
 __global__ void __launch_bounds__(128, VC_SH_MINB) shade_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
                                                        const float4* __restrict__ grad, RayPos rp0,
                                                        const uint8_t* __restrict__ dist, int mx, int my,
-                                                       int skip_on, uchar4* __restrict__ out,
+                                                       int skip_on, PixelSink sink,
                                                        unsigned long long* counters, FrameWork* work,
                                                        const HitEntry* __restrict__ hits) {
     const unsigned FULL = 0xffffffffu;
@@ -714,7 +736,7 @@ __global__ void __launch_bounds__(128, VC_SH_MINB) shade_kernel(const __grid_con
                 fin = shade_and_composite<T, OP, INTERP>(C, P, R, R.t_hit, o, nshade);
             }
             if (fin) {
-                out[(size_t)lr * P.width + px] = o;
+                put_pixel(sink, P, lr, px, o);
                 active = false;
             }
         }
@@ -755,10 +777,11 @@ static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
     cudaError_t e = cudaMemsetAsync(fw, 0, sizeof(FrameWork), stream);
     if (e != cudaSuccess) return e;
     const long long tiles = (long long)((L.p->width + 7) / 8) * ((L.local_rows + 3) / 4);
+    PixelSink sink{reinterpret_cast<uchar4*>(L.out), reinterpret_cast<uchar4* const*>(L.peers), L.npeers};
     if (L.ev[0]) cudaEventRecord(L.ev[0], stream);
     firsthit_kernel<T, OP, INTERP><<<persistent_blocks(firsthit_kernel<T, OP, INTERP>, (tiles + 3) / 4), 128, 0,
-                                     stream>>>(*L.p, vol, L.rp, L.occ, L.mx, L.my, L.skip_on,
-                                               reinterpret_cast<uchar4*>(L.out), L.local_rows,
+                                     stream>>>(*L.p, vol, L.rp, L.occ, L.mx, L.my, L.skip_on, sink,
+                                               L.local_rows,
                                                reinterpret_cast<unsigned long long*>(L.counters), fw, hits,
                                                L.oct);
     e = cudaGetLastError();
@@ -766,7 +789,7 @@ static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
     if (L.ev[1]) cudaEventRecord(L.ev[1], stream);
     shade_kernel<T, OP, INTERP><<<persistent_blocks(shade_kernel<T, OP, INTERP>, (tiles + 3) / 4), 128, 0,
                                   stream>>>(*L.p, vol, static_cast<const float4*>(L.grad), L.rp, L.occ, L.mx,
-                                            L.my, L.skip_on, reinterpret_cast<uchar4*>(L.out),
+                                            L.my, L.skip_on, sink,
                                             reinterpret_cast<unsigned long long*>(L.counters), fw, hits);
     if (L.ev[2]) cudaEventRecord(L.ev[2], stream);
     return cudaGetLastError();

@@ -39,7 +39,9 @@ struct RenderLaunch {
     const uint8_t* occ;   // macrocell occupancy for the current window
     int mx, my;
     int skip_on;
-    uint8_t* out;         // local_rows x width x 4
+    uint8_t* out;         // local_rows x width x 4 (npeers == 0)
+    void* const* peers;   // device array of npeers full-frame buffers (fused gather)
+    int npeers;
     int local_rows;
     uint64_t* counters;   // VC_NUM_COUNTERS or nullptr
     void* work;           // frame work counters (FrameWork, zeroed per launch)

@@ -76,3 +76,63 @@ def test_band_plan_covers_every_row_once():
             r * plan.max_rows + i for r in range(world) for i in range(len(plan.rows_of[r])))
     with pytest.raises(ValueError):
         BandPlan(10, 4, 0, 2, 0)
+
+
+class FakeIpc:
+    """Stand-in for CUDA IPC: 'allocations' are ids, handles are bytes."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.opened = []
+
+    def alloc(self, nbytes):
+        return 1000 + self.rank
+
+    def free(self, ptr):
+        pass
+
+    def handle(self, ptr):
+        return f"rank{self.rank}:{ptr}".encode().ljust(64, b"\0")
+
+    def open(self, handle):
+        tag = handle.rstrip(b"\0").decode()
+        ptr = int(tag.split(":")[1]) + 10_000  # distinct mapping address
+        self.opened.append(tag)
+        return ptr
+
+    def close(self, ptr):
+        pass
+
+
+def _peer_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1609_01317_b200.dispatch import PeerFrames
+
+        ipc = FakeIpc(rank)
+        pf = PeerFrames(36, 20, device=0, ipc=ipc)
+        q.put((rank, pf.peer_ptrs, sorted(ipc.opened)))
+        pf.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_peer_frame_handle_exchange():
+    """Every rank maps every other rank's frame buffer exactly once and keeps
+    its own allocation at its own slot of the pointer table."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=5) for _ in range(world))
+    for rank, ptrs, opened in res:
+        assert ptrs[rank] == 1000 + rank
+        assert [p for r, p in enumerate(ptrs) if r != rank] == [1000 + r + 10_000 for r in range(world) if r != rank]
+        assert opened == sorted(f"rank{r}:{1000 + r}" for r in range(world) if r != rank)

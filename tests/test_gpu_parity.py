@@ -324,3 +324,30 @@ def test_degenerate_grids_vs_oracle(shape, mode):
         assert np.array_equal(fb.pixels, want) and fb.sample_count == cnt, (shape, op)
         fb = vc.render_frame(vol, sc, product_settings_from(st, use_octree=True, gradient_source="volume"))
         assert maxdiff(fb.pixels, want) <= 1
+
+
+@pytest.mark.parametrize("gather", ["nccl", "peer"])
+def test_distributed_render_single_rank(gather):
+    """render_frame_distributed on a 1-rank NCCL group: the band plan, the
+    fused peer-store path (vc_render_to_peers) and the NCCL path reproduce
+    render_frame bit-exactly."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1609_01317_b200.dispatch import render_frame_distributed
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        vol = phantoms.ct_phantom(96)
+        sc, st = phantoms.scene_c3(vol, width=200, height=117, azimuth=12.0)
+        want = vc.render_frame(vol, sc, st)
+        got = render_frame_distributed(vol, sc, st, band_rows=8, gather=gather)
+        assert np.array_equal(got.pixels, want.pixels)
+        assert got.sample_count == want.sample_count
+    finally:
+        dist.destroy_process_group()
