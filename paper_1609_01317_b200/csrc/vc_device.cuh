@@ -30,7 +30,16 @@ constexpr double INV_SQRT3 = 0x1.279a74590331dp-1;  // 0.5773502691896258
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+// IEEE division.  A zero numerator (frequent: hu = (v - mu)/mu on voxels
+// equal to mu_water) takes the slow, divergent branch of __ddiv_rn; 0 / b
+// is +-0 with the xor of the signs for every finite non-zero b, which
+// 0 * copysign(1, b) reproduces exactly.
+__device__ __forceinline__ double ddiv(double a, double b) {
+#ifndef VC_DDIV_PLAIN
+    if (a == 0.0 && b != 0.0 && fabs(b) < 1.0 / 0.0) return __dmul_rn(a, copysign(1.0, b));
+#endif
+    return __ddiv_rn(a, b);
+}
 
 // _kernels.py:35-37
 __device__ __forceinline__ double lerp(double f0, double f1, double t) {
@@ -501,7 +510,10 @@ __device__ __forceinline__ bool grad_raw_shared(const Vol<T>& v, double x, doubl
 
 // _kernels.py:180-185
 __device__ __forceinline__ void normalize3(const double g[3], double u[3]) {
-    const double n = __dsqrt_rn(dadd(dadd(dmul(g[0], g[0]), dmul(g[1], g[1])), dmul(g[2], g[2])));
+    const double s = dadd(dadd(dmul(g[0], g[0]), dmul(g[1], g[1])), dmul(g[2], g[2]));
+    // zero gradients (flat regions, frequent) would take the slow sqrt path;
+    // sqrt(0) = 0 <= eps gives the zero vector either way
+    const double n = s == 0.0 ? 0.0 : __dsqrt_rn(s);
     if (n <= GRAD_EPS) {
         u[0] = u[1] = u[2] = 0.0;
         return;
