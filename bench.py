@@ -476,6 +476,10 @@ def run_ours(args):
     alg_frame = 8 * bpv * w_frame + 128 * k_frame + 4 * H * W
     alg_stage = [8 * bpv * bf[4], 8 * bpv * (bf[5] + k_frame) + 128 * k_frame + 4 * H * W]
     dom = int(np.argmax(stage))
+    # sample roofline: the march's own unit of work at its measured ceiling
+    peak_gs = ctypes.c_double(0.0)
+    _native.check(L.vc_sample_peak(dev, ctypes.byref(peak_gs)))
+    exec_samples_per_s = (float(ce[0]) + float(ce[1])) / (float(np.sum(stage)) / 1000.0) / 1e9
     names = ["vc::firsthit_kernel", "vc::shade_kernel"]
     peak, peak_kind = peaks()
     achieved = alg_stage[dom] / (stage[dom] / 1000.0) / 1e9
@@ -508,6 +512,12 @@ def run_ours(args):
                      "note": "logical bytes 8*bpv per ray sample + 128 per shade + 4 per pixel "
                              "(SURVEY.md 8(d)), brute-force counts; the kernels are L1-gather/FP64 "
                              "bound, HBM is the stated denominator"},
+        "sample_roofline": {"bound": "L1-resident float64 ray samples (vc_sample_peak)",
+                            "peak_gsamples_per_s": peak_gs.value,
+                            "achieved_executed_gsamples_per_s": exec_samples_per_s,
+                            "frac": exec_samples_per_s / peak_gs.value if peak_gs.value else None,
+                            "note": "executed samples + shades of both stages over their summed "
+                                    "device time; a shade costs far more than one sample"},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": 2 * args.steps,

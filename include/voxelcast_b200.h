@@ -207,6 +207,11 @@ VC_API int vc_render_profiled(vc_volume *vol, const vc_render_params *p, uint8_t
 VC_API int vc_render_host(vc_volume *vol, const vc_render_params *p, uint8_t *h_rgba,
                    uint64_t *h_counters, float *ms);
 
+/* Measured ceiling of the march's unit of work on `device`: float64 ray
+ * samples per second (Gsamples/s) with all data L1-resident and no
+ * divergence -- the "sample roofline" reported beside the HBM one. */
+VC_API int vc_sample_peak(int device, double *gsamples_per_s);
+
 /* Point queries backing the public sampling / gradient API, host arrays.
  *   vc_sample_points   -> volume.sample / _kernels.sample_any (volume.py:104-110)
  *   vc_gradient_points -> _kernels.grad_raw (gradients.py:79-83), raw (N,3)  */
