@@ -62,7 +62,10 @@ cudaError_t launch_gradient_prepass(int dtype, const void* data, int nx, int ny,
 cudaError_t launch_macrocell_minmax(int dtype, const void* data, int nx, int ny, int nz, float2* mm,
                                     int mx, int my, int mz, cudaStream_t s);
 // occupancy of [lo, hi] + its Chebyshev distance field (dist: 0 = occupied)
-constexpr int DIST_PASSES = 16;
+#ifndef VC_DIST_PASSES
+#define VC_DIST_PASSES 16
+#endif
+constexpr int DIST_PASSES = VC_DIST_PASSES;  // max jump = (DIST_PASSES + 1) macrocells
 cudaError_t launch_occupancy(const float2* mm, int mx, int my, int mz, double lo, double hi, uint8_t* dist,
                              uint8_t* scratch, cudaStream_t s);
 
