@@ -207,6 +207,13 @@ VC_API int vc_render_profiled(vc_volume *vol, const vc_render_params *p, uint8_t
 VC_API int vc_render_host(vc_volume *vol, const vc_render_params *p, uint8_t *h_rgba,
                    uint64_t *h_counters, float *ms);
 
+/* Frame egress (image_io.png_bytes, image_io.py:52-55): encode a device
+ * RGBA frame (height x width x 4, row-major) as an 8-bit RGB PNG on the
+ * device and copy only the compressed file into h_out (capacity h_cap);
+ * *out_len = file size.  h_out == NULL: size query.  Synchronous on stream. */
+VC_API int vc_encode_png(const uint8_t *d_rgba, int width, int height, void *stream, uint8_t *h_out,
+                         size_t h_cap, size_t *out_len);
+
 /* Measured ceiling of the march's unit of work on `device`: float64 ray
  * samples per second (Gsamples/s) with all data L1-resident and no
  * divergence -- the "sample roofline" reported beside the HBM one. */

@@ -38,7 +38,7 @@ EXPORTS = (
     "vc_gradient_prepass", "vc_gradient_volume", "vc_gradient_prepass_into",
     "vc_render", "vc_render_profiled", "vc_render_host", "vc_render_to_peers",
     "vc_ipc_handle", "vc_ipc_open", "vc_ipc_close", "vc_device_alloc", "vc_device_free",
-    "vc_memcpy_to_host", "vc_sample_peak",
+    "vc_memcpy_to_host", "vc_sample_peak", "vc_encode_png",
     "vc_sample_points", "vc_gradient_points",
     "vc_box_interval_rays", "vc_first_hit_rays", "vc_bisect_rays",
 )
@@ -134,6 +134,8 @@ def load(build_if_missing: bool = True):
             "vc_device_alloc": ([ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(vp)], ctypes.c_int),
             "vc_device_free": ([vp], ctypes.c_int),
             "vc_sample_peak": ([ctypes.c_int, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+            "vc_encode_png": ([vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t,
+                               ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
             "vc_memcpy_to_host": ([vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
             "vc_ipc_handle": ([vp, vp], ctypes.c_int),
             "vc_ipc_open": ([ctypes.c_int, vp, ctypes.POINTER(vp)], ctypes.c_int),

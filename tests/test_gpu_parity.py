@@ -351,3 +351,55 @@ def test_distributed_render_single_rank(gather):
         assert got.sample_count == want.sample_count
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("wh", [(1920, 1080), (257, 3), (1, 1), (640, 480)])
+def test_device_png_round_trip(wh):
+    """Frame egress: the device PNG decodes (zlib, CRC and Adler-32 checked
+    by the decoders) to exactly the frame's RGB (image_io.png_bytes drops
+    alpha the same way)."""
+    import io
+    import zlib
+
+    from PIL import Image
+
+    from paper_1609_01317_b200 import egress
+
+    W, H = wh
+    rng = np.random.default_rng(W * 7 + H)
+    img = np.zeros((H, W, 4), np.uint8)
+    img[..., 3] = 255
+    img[H // 3:, : max(W // 2, 1), :3] = rng.integers(0, 256, (H - H // 3, max(W // 2, 1), 3))
+    img[: H // 4, :, 0] = 200  # long runs
+    png = egress.png_bytes(img)
+    assert png[:8] == b"\x89PNG\r\n\x1a\n"
+    dec = np.asarray(Image.open(io.BytesIO(png)).convert("RGB"))
+    assert np.array_equal(dec, img[..., :3])
+    # the IDAT payload is a valid zlib stream
+    pos = 8
+    while pos < len(png):
+        n = int.from_bytes(png[pos:pos + 4], "big")
+        typ = png[pos + 4:pos + 8]
+        if typ == b"IDAT":
+            raw = zlib.decompress(png[pos + 8:pos + 8 + n])
+            assert len(raw) == H * (1 + 3 * W)
+        pos += 12 + n
+
+
+def test_render_frame_png_matches_render_frame():
+    import io
+
+    from PIL import Image
+
+    from paper_1609_01317_b200 import egress
+
+    vol = phantoms.ct_phantom(128)
+    sc, st = phantoms.scene_c3(vol, width=480, height=270, azimuth=21.0)
+    fb = vc.render_frame(vol, sc, st)
+    png, meta = egress.render_frame_png(vol, sc, st)
+    dec = np.asarray(Image.open(io.BytesIO(png)).convert("RGB"))
+    assert np.array_equal(dec, fb.pixels[..., :3])
+    assert meta.sample_count == fb.sample_count and meta.pixels is None
+    assert len(png) < fb.pixels[..., :3].nbytes / 2  # it compresses
+    pkt = egress.frame_packet(7, png)
+    assert int.from_bytes(pkt[:8], "big") == 7 and int.from_bytes(pkt[8:12], "big") == len(png)
