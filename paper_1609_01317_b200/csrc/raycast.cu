@@ -23,6 +23,7 @@
 //   * warp-vote retirement: per-warp sample / shade counters are reduced
 //     with __reduce_add_sync and committed with one atomic per warp.
 #include <cfloat>
+#include <type_traits>
 
 #include "vc_device.cuh"
 #include "vc_internal.h"
@@ -150,10 +151,25 @@ __device__ __forceinline__ bool window_at(const Ctx<T>& C, const vc_render_param
 }
 
 // Trilinear interpolation of the packed gradient volume at an interior
-// point; also returns the trilinear value from the .w channel, which is
-// bit-identical to sample_trilinear (same operands, same order).
+// point.  The value comes from the .w channel in float64 and is
+// bit-identical to sample_trilinear (same operands, same order), so the
+// opacity, the transmittance and every early-termination decision stay the
+// reference's.  The gradient only feeds the diffuse term; it is stored in
+// float32 and interpolated in float32 (the float64 lerps of float32 data
+// bought nothing: the stored values already carry the float32 rounding).
+template <typename T>
+__device__ __forceinline__ double w_to_double(float w) {
+    if constexpr (std::is_integral<T>::value) {
+        // .w holds an exact integer <= 65535: w + 2^23 has it as mantissa
+        return u2d(__float_as_uint(__fadd_rn(w, 8388608.0f)) & 0x7fffffu);
+    } else {
+        return (double)w;
+    }
+}
+
+template <typename T>
 __device__ __forceinline__ void grad_from_volume(const float4* __restrict__ G, int nx, int ny,
-                                                 const double p[3], double g[3], double& value) {
+                                                 const double p[3], float g[3], double& value) {
     double fx, fy, fz;
     double r;  // interior point: no clamping
     const int i0 = floor_pos(p[0], r);
@@ -167,17 +183,20 @@ __device__ __forceinline__ void grad_from_volume(const float4* __restrict__ G, i
     const float4 c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + sy), c110 = __ldg(b + sy + 1);
     const float4 c001 = __ldg(b + sz), c101 = __ldg(b + sz + 1), c011 = __ldg(b + sz + sy),
                  c111 = __ldg(b + sz + sy + 1);
-#define VC_TRI(comp)                                                                   \
-    lerp(lerp(lerp((double)c000.comp, (double)c100.comp, fx),                          \
-              lerp((double)c010.comp, (double)c110.comp, fx), fy),                     \
-         lerp(lerp((double)c001.comp, (double)c101.comp, fx),                          \
-              lerp((double)c011.comp, (double)c111.comp, fx), fy),                     \
-         fz)
-    g[0] = VC_TRI(x);
-    g[1] = VC_TRI(y);
-    g[2] = VC_TRI(z);
-    value = VC_TRI(w);
-#undef VC_TRI
+    const float ffx = (float)fx, ffy = (float)fy, ffz = (float)fz;
+#define VC_LF(a, b, t) fmaf((b) - (a), (t), (a))
+#define VC_TRIF(comp)                                                                          \
+    VC_LF(VC_LF(VC_LF(c000.comp, c100.comp, ffx), VC_LF(c010.comp, c110.comp, ffx), ffy),     \
+          VC_LF(VC_LF(c001.comp, c101.comp, ffx), VC_LF(c011.comp, c111.comp, ffx), ffy), ffz)
+    g[0] = VC_TRIF(x);
+    g[1] = VC_TRIF(y);
+    g[2] = VC_TRIF(z);
+#undef VC_TRIF
+#undef VC_LF
+#define VC_W(c) w_to_double<T>(c.w)
+    value = lerp(lerp(lerp(VC_W(c000), VC_W(c100), fx), lerp(VC_W(c010), VC_W(c110), fx), fy),
+                 lerp(lerp(VC_W(c001), VC_W(c101), fx), lerp(VC_W(c011), VC_W(c111), fx), fy), fz);
+#undef VC_W
 }
 
 #ifdef VC_DEBUG_TAPS
@@ -221,34 +240,43 @@ __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_pa
     p[0] = dsub(r.pow2 ? dmul(wx, r.rs[0]) : ddiv(wx, r.s[0]), 0.5);
     p[1] = dsub(r.pow2 ? dmul(wy, r.rs[1]) : ddiv(wy, r.s[1]), 0.5);
     p[2] = dsub(r.pow2 ? dmul(wz, r.rs[2]) : ddiv(wz, r.s[2]), 0.5);
-    double val, g[3];
+    double val, illum = 0.0;
     const bool interior = p[0] >= 1.0 && p[0] <= dsub(C.v.mx, 1.0) && p[1] >= 1.0 &&
                           p[1] <= dsub(C.v.my, 1.0) && p[2] >= 1.0 && p[2] <= dsub(C.v.mz, 1.0);
     if (C.grad != nullptr && interior) {
+        // diffuse term in float32 from the stored float32 gradient:
+        // illum = dot(L, -g) / (|L| |g|), 0 for |g| <= EPS_GRADIENT or |L| = 0
+        float g[3];
         double gv;
-        grad_from_volume(C.grad, C.v.nx, C.v.ny, p, g, gv);
+        grad_from_volume<T>(C.grad, C.v.nx, C.v.ny, p, g, gv);
         val = (INTERP == VC_TRILINEAR) ? gv : sample_any<T, INTERP>(C.v, p[0], p[1], p[2]);
+        const float lx = (float)dsub(P.light_pos[0], wx);
+        const float ly = (float)dsub(P.light_pos[1], wy);
+        const float lz = (float)dsub(P.light_pos[2], wz);
+        const float g2 = fmaf(g[0], g[0], fmaf(g[1], g[1], g[2] * g[2]));
+        const float l2 = fmaf(lx, lx, fmaf(ly, ly, lz * lz));
+        if (g2 > 1e-16f && l2 > 0.0f) {
+            const float d = -fmaf(lx, g[0], fmaf(ly, g[1], lz * g[2]));
+            illum = (double)(d * rsqrtf(g2) * rsqrtf(l2));
+        }
     } else {
 #ifdef VC_DEBUG_TAPS
         if (C.grad != nullptr) atomicAdd(&g_debug_taps, 1u);
 #endif
         const double4 gg = grad_taps<T, OP>(C.v, p[0], p[1], p[2]);
-        g[0] = gg.x;
-        g[1] = gg.y;
-        g[2] = gg.z;
+        double g[3] = {gg.x, gg.y, gg.z};
         // the footprint's centre is sample_trilinear(p) (bit-identical)
         val = (INTERP == VC_TRILINEAR && gg.w == gg.w) ? gg.w : sample_any<T, INTERP>(C.v, p[0], p[1], p[2]);
+        double u[3];
+        normalize3(g, u);
+        // field values rise toward the interior, the surface normal points away
+        const double snx = -u[0], sny = -u[1], snz = -u[2];
+        const double lx = dsub(P.light_pos[0], wx);
+        const double ly = dsub(P.light_pos[1], wy);
+        const double lz = dsub(P.light_pos[2], wz);
+        const double ln = __dsqrt_rn(dadd(dadd(dmul(lx, lx), dmul(ly, ly)), dmul(lz, lz)));
+        if (ln > 0.0) illum = ddiv(dadd(dadd(dmul(lx, snx), dmul(ly, sny)), dmul(lz, snz)), ln);
     }
-    double u[3];
-    normalize3(g, u);
-    // field values rise toward the interior, the surface normal points away
-    const double snx = -u[0], sny = -u[1], snz = -u[2];
-    const double lx = dsub(P.light_pos[0], wx);
-    const double ly = dsub(P.light_pos[1], wy);
-    const double lz = dsub(P.light_pos[2], wz);
-    const double ln = __dsqrt_rn(dadd(dadd(dmul(lx, lx), dmul(ly, ly)), dmul(lz, lz)));
-    double illum = 0.0;
-    if (ln > 0.0) illum = ddiv(dadd(dadd(dmul(lx, snx), dmul(ly, sny)), dmul(lz, snz)), ln);
     illum = clamp01(illum);
     const double hu = dmul(ddiv(dsub(val, P.mu_water), P.mu_water), 1000.0);
     double m[4];
