@@ -55,6 +55,10 @@ struct Vol {
     double mx, my, mz, cx, cy, cz;
     // max |voxel value| (bounds the float32 pre-test error); <= 0: unknown
     double amax;
+    // max(n-2, 0): the clamped lower cell corner; element offsets of the
+    // +1 corner along x / y / z (0 on a one-voxel axis, _kernels.py:53-64)
+    int kx, ky, kz;
+    uint32_t sx1, sy1, sz1;
 };
 
 template <typename T>
@@ -71,6 +75,12 @@ __host__ __device__ inline Vol<T> make_vol(const T* data, int nx, int ny, int nz
     v.cx = (double)(nx - 2 < 0 ? 0 : nx - 2);
     v.cy = (double)(ny - 2 < 0 ? 0 : ny - 2);
     v.cz = (double)(nz - 2 < 0 ? 0 : nz - 2);
+    v.kx = nx - 2 < 0 ? 0 : nx - 2;
+    v.ky = ny - 2 < 0 ? 0 : ny - 2;
+    v.kz = nz - 2 < 0 ? 0 : nz - 2;
+    v.sx1 = nx > 1 ? 1u : 0u;
+    v.sy1 = ny > 1 ? (uint32_t)nx : 0u;
+    v.sz1 = nz > 1 ? (uint32_t)nx * (uint32_t)ny : 0u;
     return v;
 }
 
@@ -209,34 +219,30 @@ struct Loc {
     double fx, fy, fz;  // fractions v - i0
 };
 
-__device__ __forceinline__ bool locate_axis(double x, int n, double nm1, double nm2, int& i0, double& f) {
-    double r;
-    int i = floor_pos(x, r);  // exact floor for negative x too
-    // in range  <=>  0 <= x <= n-1  <=>  i >= 0 and (i <= n-2 or x == n-1)
-    const bool inr = i >= 0 && (i <= n - 2 || x == nm1);
-    if (i > n - 2) {
-        i = n - 2 < 0 ? 0 : n - 2;
-        r = nm2;
-    }
+// n1 = n-1, kmax = max(n-2, 0), nm1 = (double)(n-1).  L (i0, f) is only
+// meaningful when the result is true.
+__device__ __forceinline__ bool locate_axis(double x, int n1, int kmax, double nm1, int& i0, double& f) {
+    int i = __double2int_rd(x);  // F2I.F64.FLOOR, exact for negative x too
+    // in range  <=>  0 <= x <= n-1  <=>  0 <= i < n-1, or x == n-1
+    const bool inr = (uint32_t)i < (uint32_t)n1 || x == nm1;
+    i = min(i, kmax);            // the clamp of _kernels.py:53-64 (x == n-1)
     i0 = i;
-    f = dsub(x, r);
+    f = dsub(x, biased2d((uint32_t)i + 0x80000000u));
     return inr;
 }
 
 template <typename T>
 __device__ __forceinline__ bool locate(const Vol<T>& v, const double p[3], Loc& L) {
-    const bool a = locate_axis(p[0], v.nx, v.mx, v.cx, L.i, L.fx);
-    const bool b = locate_axis(p[1], v.ny, v.my, v.cy, L.j, L.fy);
-    const bool c = locate_axis(p[2], v.nz, v.mz, v.cz, L.k, L.fz);
+    const bool a = locate_axis(p[0], v.nx - 1, v.kx, v.mx, L.i, L.fx);
+    const bool b = locate_axis(p[1], v.ny - 1, v.ky, v.my, L.j, L.fy);
+    const bool c = locate_axis(p[2], v.nz - 1, v.kz, v.mz, L.k, L.fz);
     return a && b && c;
 }
 
 // sample_trilinear (_kernels.py:104-115) from a precomputed in-range Loc
 template <typename T>
 __device__ __forceinline__ double trilinear_at(const Vol<T>& v, const Loc& L) {
-    const uint32_t sx = L.i + 1 < v.nx ? 1u : 0u;
-    const uint32_t sy = L.j + 1 < v.ny ? (uint32_t)v.nx : 0u;
-    const uint32_t sz = L.k + 1 < v.nz ? (uint32_t)v.nx * (uint32_t)v.ny : 0u;
+    const uint32_t sx = v.sx1, sy = v.sy1, sz = v.sz1;  // L is clamped: i+1 < n unless n == 1
     const T* b = v.data + (((uint32_t)L.k * (uint32_t)v.ny + (uint32_t)L.j) * (uint32_t)v.nx + (uint32_t)L.i);
     const T c000 = ldv(b), c100 = ldv(b + sx), c010 = ldv(b + sy), c110 = ldv(b + sy + sx);
     const T c001 = ldv(b + sz), c101 = ldv(b + sz + sx), c011 = ldv(b + sz + sy),
@@ -291,9 +297,7 @@ __device__ __forceinline__ float vox_f32(T c) {
 template <typename T>
 __device__ __forceinline__ bool in_window_trilinear(const Vol<T>& v, const Loc& L, double t_low, double t_high,
                                                     const WinF& w) {
-    const uint32_t sx = L.i + 1 < v.nx ? 1u : 0u;
-    const uint32_t sy = L.j + 1 < v.ny ? (uint32_t)v.nx : 0u;
-    const uint32_t sz = L.k + 1 < v.nz ? (uint32_t)v.nx * (uint32_t)v.ny : 0u;
+    const uint32_t sx = v.sx1, sy = v.sy1, sz = v.sz1;  // L is clamped: i+1 < n unless n == 1
     const T* b = v.data + (((uint32_t)L.k * (uint32_t)v.ny + (uint32_t)L.j) * (uint32_t)v.nx + (uint32_t)L.i);
     const T c000 = ldv(b), c100 = ldv(b + sx), c010 = ldv(b + sy), c110 = ldv(b + sy + sx);
     const T c001 = ldv(b + sz), c101 = ldv(b + sz + sx), c011 = ldv(b + sz + sy),

@@ -88,7 +88,7 @@ def main():
         t = np.array(times)
         print(f"{name:28s} {t.mean():7.3f} ms (min {t.min():.3f}, max {t.max():.3f})  "
               f"fps {1000 / t.mean():7.1f}  samples {c[0]/1e6:6.2f}M shades {c[1]/1e6:5.2f}M "
-              f"skipped {c[2]/1e6:6.1f}M{diff}", flush=True)
+              f"skipped {c[2]/1e6:6.1f}M st1 {c[4]/1e6:6.2f}M st2 {c[5]/1e6:6.2f}M{diff}", flush=True)
 
 
 if __name__ == "__main__":
