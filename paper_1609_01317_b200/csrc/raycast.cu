@@ -230,7 +230,9 @@ __device__ __noinline__ double4 grad_taps(Vol<T> v, double x, double y, double z
 }
 
 // _kernels.py:528-579
-template <typename T, int OP, int INTERP>
+// GV: shading gradient from the packed volume (C.grad != nullptr) -- a
+// template parameter so the taps-only kernel carries none of that code
+template <typename T, int OP, int INTERP, bool GV>
 __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_params& P, double t) {
     const RayPos& r = C.rp;
     const double wx = dadd(r.o[0], dmul(t, r.d[0]));
@@ -243,7 +245,7 @@ __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_pa
     double val, illum = 0.0;
     const bool interior = p[0] >= 1.0 && p[0] <= dsub(C.v.mx, 1.0) && p[1] >= 1.0 &&
                           p[1] <= dsub(C.v.my, 1.0) && p[2] >= 1.0 && p[2] <= dsub(C.v.mz, 1.0);
-    if (C.grad != nullptr && interior) {
+    if (GV && interior) {
         // diffuse term in float32 from the stored float32 gradient:
         // illum = dot(L, -g) / (|L| |g|), 0 for |g| <= EPS_GRADIENT or |L| = 0
         float g[3];
@@ -261,7 +263,7 @@ __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_pa
         }
     } else {
 #ifdef VC_DEBUG_TAPS
-        if (C.grad != nullptr) atomicAdd(&g_debug_taps, 1u);
+        if (GV) atomicAdd(&g_debug_taps, 1u);
 #endif
         const double4 gg = grad_taps<T, OP>(C.v, p[0], p[1], p[2]);
         double g[3] = {gg.x, gg.y, gg.z};
@@ -485,10 +487,10 @@ __device__ __forceinline__ uchar4 composite_pixel(const vc_render_params& P, con
 // the first shade's acc = a*c, remain = 1 - a come out bit-identical to the
 // reference (_kernels.py:744-754: 1.0*a*c == a*c, 0.0 + x == x,
 // 1.0*(1-a) == 1-a).  Returns true when the pixel is finished.
-template <typename T, int OP, int INTERP>
+template <typename T, int OP, int INTERP, bool GV>
 __device__ __forceinline__ bool shade_and_composite(const Ctx<T>& C, const vc_render_params& P, RayState& R,
                                                     double tcur, uchar4& out, unsigned& nshade) {
-    const Rgba s = shade_sample<T, OP, INTERP>(C, P, tcur);
+    const Rgba s = shade_sample<T, OP, INTERP, GV>(C, P, tcur);
     nshade++;
     if (P.mode == VC_SURFACE) {
         out = make_uchar4(quant(s.r), quant(s.g), quant(s.b), 255);
@@ -513,6 +515,9 @@ __device__ __forceinline__ bool shade_and_composite(const Ctx<T>& C, const vc_re
 #endif
 #ifndef VC_SH_READY
 #define VC_SH_READY 2
+#endif
+#ifndef VC_SHV_READY  // shade stage, gradient-volume kernel
+#define VC_SHV_READY 1
 #endif
 constexpr int READY_DEN = 4;
 
@@ -616,6 +621,9 @@ __device__ __forceinline__ unsigned warp_ticket(unsigned* ctr, bool want) {
 #ifndef VC_SH_MINB
 #define VC_SH_MINB 5
 #endif
+#ifndef VC_SHV_MINB
+#define VC_SHV_MINB 7
+#endif
 
 template <typename T, int OP, int INTERP>
 __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
@@ -697,8 +705,8 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
 // composited mode, keep marching t_star + m*coarse and shading in-window
 // samples until early ray termination or the ray leaves the box.  Lanes
 // refill from the queue as their pixel finishes.
-template <typename T, int OP, int INTERP>
-__global__ void __launch_bounds__(128, VC_SH_MINB) shade_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
+template <typename T, int OP, int INTERP, bool GV>
+__global__ void __launch_bounds__(128, GV ? VC_SHV_MINB : VC_SH_MINB) shade_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
                                                        const float4* __restrict__ grad, RayPos rp0,
                                                        const uint8_t* __restrict__ dist, int mx, int my,
                                                        int skip_on, PixelSink sink,
@@ -750,7 +758,7 @@ __global__ void __launch_bounds__(128, VC_SH_MINB) shade_kernel(const __grid_con
             const unsigned mneed = __ballot_sync(FULL, need);
             if (mneed == 0) break;
             const unsigned mact = __ballot_sync(FULL, active);
-            if (__popc(mact & ~mneed) * READY_DEN >= __popc(mact) * VC_SH_READY) break;
+            if (__popc(mact & ~mneed) * READY_DEN >= __popc(mact) * (GV ? VC_SHV_READY : VC_SH_READY)) break;
             if (need) march_step<T, INTERP>(C, P, R, nsamp, nskip);
         }
         if (active && (R.found || R.exhausted)) {
@@ -761,7 +769,7 @@ __global__ void __launch_bounds__(128, VC_SH_MINB) shade_kernel(const __grid_con
                 fin = true;
             } else {
                 R.found = false;
-                fin = shade_and_composite<T, OP, INTERP>(C, P, R, R.t_hit, o, nshade);
+                fin = shade_and_composite<T, OP, INTERP, GV>(C, P, R, R.t_hit, o, nshade);
             }
             if (fin) {
                 put_pixel(sink, P, lr, px, o);
@@ -815,10 +823,16 @@ static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (L.ev[1]) cudaEventRecord(L.ev[1], stream);
-    shade_kernel<T, OP, INTERP><<<persistent_blocks(shade_kernel<T, OP, INTERP>, (tiles + 3) / 4), 128, 0,
-                                  stream>>>(*L.p, vol, static_cast<const float4*>(L.grad), L.rp, L.occ, L.mx,
-                                            L.my, L.skip_on, sink,
-                                            reinterpret_cast<unsigned long long*>(L.counters), fw, hits);
+    const float4* grad = static_cast<const float4*>(L.grad);
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(L.counters);
+    if (grad != nullptr)
+        shade_kernel<T, OP, INTERP, true><<<persistent_blocks(shade_kernel<T, OP, INTERP, true>, (tiles + 3) / 4),
+                                            128, 0, stream>>>(*L.p, vol, grad, L.rp, L.occ, L.mx, L.my,
+                                                              L.skip_on, sink, cnt, fw, hits);
+    else
+        shade_kernel<T, OP, INTERP, false><<<persistent_blocks(shade_kernel<T, OP, INTERP, false>, (tiles + 3) / 4),
+                                             128, 0, stream>>>(*L.p, vol, grad, L.rp, L.occ, L.mx, L.my,
+                                                               L.skip_on, sink, cnt, fw, hits);
     if (L.ev[2]) cudaEventRecord(L.ev[2], stream);
     return cudaGetLastError();
 }
