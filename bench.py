@@ -453,6 +453,32 @@ def run_ours(args):
                "render_frame_sync_fps": args.steps / t_sync,
                "note": "h2d per step = the scene/camera parameter block (kernel parameters)"}
 
+    if not args.no_e2e and world > 1:
+        # end to end at N GPUs through the public multi-GPU API: every step
+        # renders the rank's bands, gathers (fused peer stores or NCCL), and
+        # copies the full frame to host memory on every rank
+        from paper_1609_01317_b200.dispatch import render_frame_distributed
+
+        gmode = "peer" if peers is not None else "nccl"
+        for i in range(2):
+            render_frame_distributed(vol, *frame(i), gather=gmode, peers=peers[0] if peers else None)
+        barrier()
+        t0 = time.perf_counter()
+        checksum = 0
+        for k in range(args.steps):
+            fb = render_frame_distributed(vol, *frame(args.warmup + k), gather=gmode,
+                                          peers=peers[0] if peers else None)
+            checksum += int(fb.pixels[H // 2, W // 2, 0])
+        barrier()
+        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": args.steps / float(t.item()), "unit": UNIT,
+               "h2d_bytes_per_step": ctypes.sizeof(_native.RenderParams),
+               "d2h_bytes_per_step": H * W * 4 + 8 * _native.NUM_COUNTERS,
+               "path": f"paper_1609_01317_b200.dispatch.render_frame_distributed(gather={gmode!r}), "
+                       "synchronous per frame, full frame to host on every rank; wall clock, max over ranks",
+               "note": "h2d per step = the scene/camera parameter block (kernel parameters)"}
+
     if peers is not None:
         torch.distributed.barrier()  # no rank still stores into a mapping we unmap
         for pf in peers:
@@ -499,7 +525,7 @@ def run_ours(args):
         "gsamples_per_s": w_frame * fps / 1e9,
         "work_per_frame": {"W_ray_samples_bruteforce": w_frame, "K_shades": k_frame,
                            "executed": {"samples": float(ce[0]), "shades": float(ce[1]),
-                                        "skipped": float(ce[2]), "rays_in_box": float(ce[3])}},
+                                        "skip_events": float(ce[2]), "rays_in_box": float(ce[3])}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
                      "traffic": (traffic or {}).get(names[dom], {}).get("dram_bytes_per_launch"),

@@ -132,7 +132,7 @@ typedef struct vc_octree_desc {
  *   [0] volume samples taken by marching, fine scan, bisection and the
  *       composite loop (each one sample_any call in the reference)
  *   [1] shades (each _shade_sample call: 1 value sample + GRAD_SAMPLES taps)
- *   [2] lattice samples skipped by empty-space skipping
+ *   [2] empty-space skip events (jumps over empty macrocells, out-of-volume samples)
  *   [3] pixels whose ray hit the volume box
  *   [4] of [0], samples taken by the first-hit stage (march, fine scan, bisection)
  *   [5] of [0], samples taken by the shade stage (composite march)

@@ -59,6 +59,8 @@ def main():
             sc, st = phantoms.scene_c3(vol, op=op, width=a.width, height=a.height, azimuth=float(i),
                                        mode=mode)
             st = replace(st, gradient_source=grad, use_octree="noskip" not in parts)
+            if "norefine" in parts:  # work accounting only: no bisection
+                st = replace(st, refine_iters=0)
             return render_params(vol, sc, st)
 
         for i in range(3):
@@ -88,7 +90,7 @@ def main():
         t = np.array(times)
         print(f"{name:28s} {t.mean():7.3f} ms (min {t.min():.3f}, max {t.max():.3f})  "
               f"fps {1000 / t.mean():7.1f}  samples {c[0]/1e6:6.2f}M shades {c[1]/1e6:5.2f}M "
-              f"skipped {c[2]/1e6:6.1f}M st1 {c[4]/1e6:6.2f}M st2 {c[5]/1e6:6.2f}M{diff}", flush=True)
+              f"skip-events {c[2]/1e6:6.1f}M st1 {c[4]/1e6:6.2f}M st2 {c[5]/1e6:6.2f}M{diff}", flush=True)
 
 
 if __name__ == "__main__":
