@@ -49,6 +49,7 @@ struct Ctx {
     const float4* __restrict__ grad;  // packed lattice gradients (may be null)
     RayPos rp;
     Skip sk;
+    const SharedLut* lut;             // shade stage: transfer breakpoints in shared memory
 };
 
 // ceil(x) for 0 <= x < 2^31 without the XU pipe
@@ -283,7 +284,7 @@ __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_pa
     illum = clamp01(illum);
     const double hu = dmul(ddiv(dsub(val, P.mu_water), P.mu_water), 1000.0);
     double m[4];
-    lut_eval(P, hu, m);
+    lut_eval(*C.lut, hu, m);
     Rgba out;
     out.r = clamp01(dmul(dmul(illum, P.light_col[0]), m[0]));
     out.g = clamp01(dmul(dmul(illum, P.light_col[1]), m[1]));
@@ -575,6 +576,7 @@ __device__ __forceinline__ void init_ctx(Ctx<T>& C, const vc_render_params& P, c
     C.sk.on = skip_on != 0;
     C.sk.inv_coarse = 1.0 / P.coarse;
     C.sk.win = make_winf(P.t_low, P.t_high, vol.amax);
+    C.lut = nullptr;
 }
 
 __device__ __forceinline__ void commit_counters(unsigned long long* counters, int stage, unsigned nsamp,
@@ -715,8 +717,11 @@ __global__ void __launch_bounds__(128, GV ? VC_SHV_MINB : VC_SH_MINB) shade_kern
                                                        const HitEntry* __restrict__ hits) {
     const unsigned FULL = 0xffffffffu;
     const unsigned total = *(volatile unsigned*)&work->hits;
+    __shared__ SharedLut s_lut;
+    load_shared_lut(P, s_lut);
     Ctx<T> C;
     init_ctx(C, P, vol, grad, rp0, dist, mx, my, skip_on);
+    C.lut = &s_lut;
     unsigned nsamp = 0, nshade = 0, nskip = 0, nhit = 0;
     RayState R;
     int px = 0, lr = 0;

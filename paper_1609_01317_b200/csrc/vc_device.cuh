@@ -597,4 +597,45 @@ __device__ __forceinline__ void lut_eval(const vc_render_params& P, double hu, d
     for (int c = 0; c < 4; c++) out[c] = lerp(P.lut_rgba[i][c], P.lut_rgba[i + 1][c], t);
 }
 
+// The same evaluation over a shared-memory copy of the breakpoints: lanes
+// of a warp sit in different LUT segments, and divergent indices into the
+// constant bank serialise, shared memory does not.
+struct SharedLut {
+    double hu[VC_MAX_LUT];
+    double rgba[VC_MAX_LUT][4];
+    int n;
+};
+
+__device__ __forceinline__ void lut_eval(const SharedLut& L, double hu, double out[4]) {
+    const int n = L.n;
+    int i;
+    if (hu <= L.hu[0]) {
+        i = 0;
+    } else if (hu >= L.hu[n - 1]) {
+        i = n - 1;
+    } else {
+        i = -1;
+    }
+    if (i >= 0) {
+#pragma unroll
+        for (int c = 0; c < 4; c++) out[c] = L.rgba[i][c];
+        return;
+    }
+    i = 0;
+    while (i + 1 < n - 1 && L.hu[i + 1] <= hu) i++;
+    const double t = ddiv(dsub(hu, L.hu[i]), dsub(L.hu[i + 1], L.hu[i]));
+#pragma unroll
+    for (int c = 0; c < 4; c++) out[c] = lerp(L.rgba[i][c], L.rgba[i + 1][c], t);
+}
+
+__device__ __forceinline__ void load_shared_lut(const vc_render_params& P, SharedLut& L) {
+    for (int k = threadIdx.x; k < P.lut_n; k += blockDim.x) {
+        L.hu[k] = P.lut_hu[k];
+#pragma unroll
+        for (int c = 0; c < 4; c++) L.rgba[k][c] = P.lut_rgba[k][c];
+    }
+    if (threadIdx.x == 0) L.n = P.lut_n;
+    __syncthreads();
+}
+
 }  // namespace vc
