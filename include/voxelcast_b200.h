@@ -38,7 +38,7 @@ extern "C" {
 #define VC_API
 #endif
 
-#define VC_ABI_VERSION 1
+#define VC_ABI_VERSION 2
 #define VC_MAX_LUT 64
 
 typedef enum {
@@ -69,6 +69,19 @@ typedef enum {
      * boundary band where the two differ */
     VC_GRAD_VOLUME = 1
 } vc_grad_source;
+
+/* how the scalar field (and, with VC_GRAD_VOLUME, the gradient) is
+ * reconstructed at a ray sample */
+typedef enum {
+    /* the reference's float64 7-lerp cascade from 8 voxel loads
+     * (_kernels.py:104-115): in-window decisions bit-exact */
+    VC_SAMPLER_SOFTWARE = 0,
+    /* hardware trilinear filtering of 3-D textures (tex3D on a cudaArray
+     * copy of the grid and of the float4 gradient volume): 8-bit filter
+     * weights, so decisions near the thresholds can differ from the
+     * reference; tolerance stated in DESIGN.md.  Trilinear only. */
+    VC_SAMPLER_TEXTURE = 1
+} vc_sampler;
 
 typedef struct vc_volume vc_volume;
 
@@ -110,6 +123,8 @@ typedef struct vc_render_params {
      * skip_empty off (the stride depends on the exact lattice sequence). */
     int32_t use_adaptive, adapt_jump;
     double detail_eps;
+    int32_t sampler;                    /* vc_sampler (ABI 2) */
+    int32_t reserved0;
 } vc_render_params;
 
 /* Min/max octree in level-grid form (see paper_1609_01317_b200/octree.py):
@@ -218,6 +233,9 @@ VC_API int vc_encode_png(const uint8_t *d_rgba, int width, int height, void *str
  * samples per second (Gsamples/s) with all data L1-resident and no
  * divergence -- the "sample roofline" reported beside the HBM one. */
 VC_API int vc_sample_peak(int device, double *gsamples_per_s);
+/* The same ceiling for the VC_SAMPLER_TEXTURE path: tex3D trilinear
+ * fetches (u16 grid, normalized float read) of an L1-resident 3-D texture. */
+VC_API int vc_sample_peak_texture(int device, double *gsamples_per_s);
 
 /* Point queries backing the public sampling / gradient API, host arrays.
  *   vc_sample_points   -> volume.sample / _kernels.sample_any (volume.py:104-110)

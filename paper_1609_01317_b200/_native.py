@@ -25,6 +25,7 @@ VC_ERR_UNSUPPORTED = 4
 
 VC_U8, VC_U16, VC_F32 = 0, 1, 2
 VC_GRAD_TAPS, VC_GRAD_VOLUME = 0, 1
+VC_SAMPLER_SOFTWARE, VC_SAMPLER_TEXTURE = 0, 1
 MAX_LUT = 64
 NUM_COUNTERS = 6
 
@@ -38,7 +39,7 @@ EXPORTS = (
     "vc_gradient_prepass", "vc_gradient_volume", "vc_gradient_prepass_into",
     "vc_render", "vc_render_profiled", "vc_render_host", "vc_render_to_peers",
     "vc_ipc_handle", "vc_ipc_open", "vc_ipc_close", "vc_device_alloc", "vc_device_free",
-    "vc_memcpy_to_host", "vc_sample_peak", "vc_encode_png",
+    "vc_memcpy_to_host", "vc_sample_peak", "vc_sample_peak_texture", "vc_encode_png",
     "vc_sample_points", "vc_gradient_points",
     "vc_box_interval_rays", "vc_first_hit_rays", "vc_bisect_rays",
 )
@@ -68,6 +69,7 @@ class RenderParams(ctypes.Structure):
         ("skip_empty", ctypes.c_int32), ("grad_source", ctypes.c_int32),
         ("use_adaptive", ctypes.c_int32), ("adapt_jump", ctypes.c_int32),
         ("detail_eps", ctypes.c_double),
+        ("sampler", ctypes.c_int32), ("reserved0", ctypes.c_int32),
     ]
 
 
@@ -134,6 +136,7 @@ def load(build_if_missing: bool = True):
             "vc_device_alloc": ([ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(vp)], ctypes.c_int),
             "vc_device_free": ([vp], ctypes.c_int),
             "vc_sample_peak": ([ctypes.c_int, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+            "vc_sample_peak_texture": ([ctypes.c_int, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
             "vc_encode_png": ([vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t,
                                ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
             "vc_memcpy_to_host": ([vp, vp, ctypes.c_size_t, vp], ctypes.c_int),

@@ -45,6 +45,9 @@ struct vc_volume {
     double vmin = 0.0, vmax = 0.0;  // value range (from the macrocell grid)
     float4* d_grad[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t grad_ready[3] = {nullptr, nullptr, nullptr};
+    // VC_SAMPLER_TEXTURE: cudaArray copies + texture objects, built lazily
+    cudaArray_t val_arr = nullptr, grad_arr[3] = {nullptr, nullptr, nullptr};
+    cudaTextureObject_t val_tex = 0, grad_tex[3] = {0, 0, 0};
     vc::OctDev oct{};  // device octree for adaptive stepping (owned buffers)
     uint8_t* d_scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -179,6 +182,12 @@ void release(vc_volume* v) {
         if (e) cudaEventDestroy(e);
     free_octree(v);
     for (auto& p : v->d_grad) cudaFree(p);
+    if (v->val_tex) cudaDestroyTextureObject(v->val_tex);
+    if (v->val_arr) cudaFreeArray(v->val_arr);
+    for (int i = 0; i < 3; i++) {
+        if (v->grad_tex[i]) cudaDestroyTextureObject(v->grad_tex[i]);
+        if (v->grad_arr[i]) cudaFreeArray(v->grad_arr[i]);
+    }
     cudaFree(v->d_scratch);
     cudaFree(v->d_counters);
     for (auto& kv : v->scratch) {
@@ -249,6 +258,52 @@ int ensure_grad(vc_volume* v, int op, cudaStream_t s) {
     return VC_OK;
 }
 
+// 3-D texture over a cudaArray copy of `src` (x fastest, elem bytes per
+// texel), hardware trilinear filtering, unnormalized coordinates (texel
+// centres at i + 0.5), clamp addressing (callers test the reference's
+// [0, n-1] range first).
+int make_texture(const vc_volume* v, const void* src, const cudaChannelFormatDesc& desc, size_t elem,
+                 bool normalized_read, cudaStream_t s, cudaArray_t* arr, cudaTextureObject_t* tex) {
+    const cudaExtent ext = make_cudaExtent(v->nx, v->ny, v->nz);
+    cudaError_t e = cudaMalloc3DArray(arr, &desc, ext, 0);
+    if (e != cudaSuccess) return fail(VC_ERR_NOMEM, std::string("cudaMalloc3DArray: ") + cudaGetErrorString(e));
+    cudaMemcpy3DParms cp{};
+    cp.srcPtr = make_cudaPitchedPtr(const_cast<void*>(src), (size_t)v->nx * elem, v->nx, v->ny);
+    cp.dstArray = *arr;
+    cp.extent = ext;
+    cp.kind = cudaMemcpyDeviceToDevice;
+    VC_CUDA(cudaMemcpy3DAsync(&cp, s));
+    cudaResourceDesc rd{};
+    rd.resType = cudaResourceTypeArray;
+    rd.res.array.array = *arr;
+    cudaTextureDesc td{};
+    td.addressMode[0] = td.addressMode[1] = td.addressMode[2] = cudaAddressModeClamp;
+    td.filterMode = cudaFilterModeLinear;
+    td.readMode = normalized_read ? cudaReadModeNormalizedFloat : cudaReadModeElementType;
+    td.normalizedCoords = 0;
+    VC_CUDA(cudaCreateTextureObject(tex, &rd, &td, nullptr));
+    return VC_OK;
+}
+
+int ensure_textures(vc_volume* v, int op, bool want_grad, cudaStream_t s) {
+    if (!v->val_tex) {
+        cudaChannelFormatDesc d = v->dtype == VC_U8    ? cudaCreateChannelDesc<unsigned char>()
+                                  : v->dtype == VC_U16 ? cudaCreateChannelDesc<unsigned short>()
+                                                       : cudaCreateChannelDesc<float>();
+        int rc = make_texture(v, v->d_data, d, dtype_size(v->dtype), v->dtype != VC_F32, s, &v->val_arr,
+                              &v->val_tex);
+        if (rc) return rc;
+    }
+    if (want_grad && !v->grad_tex[op]) {
+        int rc = make_texture(v, v->d_grad[op], cudaCreateChannelDesc<float4>(), sizeof(float4), false, s,
+                              &v->grad_arr[op], &v->grad_tex[op]);
+        if (rc) return rc;
+    }
+    // one-time copies: finish them before any stream samples the arrays
+    VC_CUDA(cudaStreamSynchronize(s));
+    return VC_OK;
+}
+
 constexpr size_t MAX_FIELDS = 8;
 
 // distance field of window [lo, hi], built on stream s if not cached
@@ -302,6 +357,12 @@ int validate_params(const vc_render_params* p, int* local_rows) {
     if (p->use_adaptive && p->adapt_jump < 1) return fail(VC_ERR_INVALID, "adaptive_factor must be >= 1");
     if (p->grad_source != VC_GRAD_TAPS && p->grad_source != VC_GRAD_VOLUME)
         return fail(VC_ERR_INVALID, "grad_source must be VC_GRAD_TAPS or VC_GRAD_VOLUME");
+    if (p->sampler != VC_SAMPLER_SOFTWARE && p->sampler != VC_SAMPLER_TEXTURE)
+        return fail(VC_ERR_INVALID, "sampler must be VC_SAMPLER_SOFTWARE or VC_SAMPLER_TEXTURE");
+    if (p->sampler == VC_SAMPLER_TEXTURE && p->interp != VC_TRILINEAR)
+        return fail(VC_ERR_INVALID, "the texture sampler is trilinear only");
+    if (p->sampler == VC_SAMPLER_TEXTURE && p->use_adaptive)
+        return fail(VC_ERR_UNSUPPORTED, "adaptive stepping runs on the software sampler only");
     const long long nb = (p->height + p->band_rows - 1) / p->band_rows;
     long long rows = 0;
     for (long long b = p->band_first; b < nb; b += p->band_step)
@@ -366,6 +427,15 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
         int rc = ensure_grad(v, p->op, s);
         if (rc) return rc;
         L.grad = v->d_grad[p->op];
+    }
+    L.tex_value = 0;
+    L.tex_grad = 0;
+    L.tex_scale = v->dtype == VC_U8 ? 255.0f : (v->dtype == VC_U16 ? 65535.0f : 1.0f);
+    if (p->sampler == VC_SAMPLER_TEXTURE) {
+        int rc = ensure_textures(v, p->op, L.grad != nullptr, s);
+        if (rc) return rc;
+        L.tex_value = v->val_tex;
+        L.tex_grad = L.grad ? v->grad_tex[p->op] : 0;
     }
     if (d_counters) VC_CUDA(cudaMemsetAsync(d_counters, 0, VC_NUM_COUNTERS * sizeof(uint64_t), s));
     if (local_rows == 0) return VC_OK;

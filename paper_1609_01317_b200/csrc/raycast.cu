@@ -23,6 +23,7 @@
 //   * warp-vote retirement: per-warp sample / shade counters are reduced
 //     with __reduce_add_sync and committed with one atomic per warp.
 #include <cfloat>
+#include <cmath>
 #include <type_traits>
 
 #include "vc_device.cuh"
@@ -43,12 +44,23 @@ struct Skip {
     WinF win;          // float32 pre-test thresholds of the window
 };
 
+// VC_SAMPLER_TEXTURE: the kernels take INTERP == VC_TEX (an internal code
+// next to the reference's 0/1/2) and sample through the texture unit
+constexpr int VC_TEX = 3;
+
+struct TexArgs {
+    cudaTextureObject_t v, g;  // scalar grid, float4 gradient volume (0: none)
+    float scale;               // undoes the normalized-float read of integer grids
+    float lo, hi;              // window thresholds rounded inward (exact test for a float value)
+};
+
 template <typename T>
 struct Ctx {
     Vol<T> v;
     const float4* __restrict__ grad;  // packed lattice gradients (may be null)
     RayPos rp;
     Skip sk;
+    TexArgs tx;
     const SharedLut* lut;             // shade stage: transfer breakpoints in shared memory
 };
 
@@ -96,13 +108,23 @@ __device__ __forceinline__ uint32_t macro_index(const Skip& sk, const Loc& L) {
            (uint32_t)(L.i >> MC_SHIFT);
 }
 
+// texture-unit trilinear value at voxel-space p (texel centres at i + 0.5)
+__device__ __forceinline__ float tex_value(const TexArgs& t, const double p[3]) {
+    return tex3D<float>(t.v, __double2float_rn(p[0]) + 0.5f, __double2float_rn(p[1]) + 0.5f,
+                        __double2float_rn(p[2]) + 0.5f) * t.scale;
+}
+__device__ __forceinline__ bool tex_in_window(const TexArgs& t, const double p[3]) {
+    const float v = tex_value(t, p);
+    return v >= t.lo && v <= t.hi;
+}
+
 // One lattice sample of the march: -1 when empty-space skipping proves it
 // out of window (k has been advanced, no fetch), else whether the
 // reference's sample_any at p lies in the threshold window (0 / 1).
 template <typename T, int INTERP>
 __device__ __forceinline__ int march_sample(const Ctx<T>& C, const vc_render_params& P, const double p[3],
                                             double t, double& k, double base, unsigned& nskip) {
-    if (INTERP != VC_TRILINEAR) {
+    if (INTERP != VC_TRILINEAR && INTERP != VC_TEX) {
         if (C.sk.on && !in_range(C.v, p[0], p[1], p[2])) {  // reads 0, outside the window
             k += 1.0;
             nskip += 1;
@@ -140,12 +162,17 @@ __device__ __forceinline__ int march_sample(const Ctx<T>& C, const vc_render_par
         }
     }
     if (!inr) return in_window(P, 0.0) ? 1 : 0;
+    if (INTERP == VC_TEX) return tex_in_window(C.tx, p) ? 1 : 0;
     return in_window_trilinear(C.v, L, P.t_low, P.t_high, C.sk.win) ? 1 : 0;
 }
 
 // is sample_any at p in the window? (fine scan, bisection)
 template <typename T, int INTERP>
 __device__ __forceinline__ bool window_at(const Ctx<T>& C, const vc_render_params& P, const double p[3]) {
+    if (INTERP == VC_TEX) {
+        if (!in_range(C.v, p[0], p[1], p[2])) return in_window(P, 0.0);
+        return tex_in_window(C.tx, p);
+    }
     if (INTERP != VC_TRILINEAR) return in_window(P, sample_any<T, INTERP>(C.v, p[0], p[1], p[2]));
     Loc L;
     if (!locate(C.v, p, L)) return in_window(P, 0.0);
@@ -251,9 +278,18 @@ __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_pa
         // diffuse term in float32 from the stored float32 gradient:
         // illum = dot(L, -g) / (|L| |g|), 0 for |g| <= EPS_GRADIENT or |L| = 0
         float g[3];
-        double gv;
-        grad_from_volume<T>(C.grad, C.v.nx, C.v.ny, p, g, gv);
-        val = (INTERP == VC_TRILINEAR) ? gv : sample_any<T, INTERP>(C.v, p[0], p[1], p[2]);
+        if (INTERP == VC_TEX) {  // one filtered float4 fetch: gradient + value
+            const float4 q = tex3D<float4>(C.tx.g, __double2float_rn(p[0]) + 0.5f,
+                                           __double2float_rn(p[1]) + 0.5f, __double2float_rn(p[2]) + 0.5f);
+            g[0] = q.x;
+            g[1] = q.y;
+            g[2] = q.z;
+            val = (double)q.w;
+        } else {
+            double gv;
+            grad_from_volume<T>(C.grad, C.v.nx, C.v.ny, p, g, gv);
+            val = (INTERP == VC_TRILINEAR) ? gv : sample_any<T, INTERP>(C.v, p[0], p[1], p[2]);
+        }
         const float lx = (float)dsub(P.light_pos[0], wx);
         const float ly = (float)dsub(P.light_pos[1], wy);
         const float lz = (float)dsub(P.light_pos[2], wz);
@@ -270,7 +306,8 @@ __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_pa
         const double4 gg = grad_taps<T, OP>(C.v, p[0], p[1], p[2]);
         double g[3] = {gg.x, gg.y, gg.z};
         // the footprint's centre is sample_trilinear(p) (bit-identical)
-        val = (INTERP == VC_TRILINEAR && gg.w == gg.w) ? gg.w : sample_any<T, INTERP>(C.v, p[0], p[1], p[2]);
+        constexpr int SI = INTERP == VC_TEX ? VC_TRILINEAR : INTERP;  // boundary band: software value
+        val = (SI == VC_TRILINEAR && gg.w == gg.w) ? gg.w : sample_any<T, SI>(C.v, p[0], p[1], p[2]);
         double u[3];
         normalize3(g, u);
         // field values rise toward the interior, the surface normal points away
@@ -564,8 +601,9 @@ struct FrameWork {
 template <typename T>
 __device__ __forceinline__ void init_ctx(Ctx<T>& C, const vc_render_params& P, const Vol<T>& vol,
                                          const float4* grad, const RayPos& rp0, const uint8_t* dist, int mx,
-                                         int my, int skip_on) {
+                                         int my, int skip_on, const TexArgs& tex) {
     C.v = vol;
+    C.tx = tex;
     C.grad = grad;
     C.rp = rp0;
 #pragma unroll
@@ -628,18 +666,18 @@ __device__ __forceinline__ unsigned warp_ticket(unsigned* ctr, bool want) {
 #define VC_SHV_MINB 7
 #endif
 
-template <typename T, int OP, int INTERP>
+template <typename T, int INTERP>
 __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
                                                           RayPos rp0, const uint8_t* __restrict__ dist, int mx,
                                                           int my, int skip_on, PixelSink sink,
                                                           int local_rows, unsigned long long* counters,
                                                           FrameWork* work, HitEntry* __restrict__ hits,
-                                                          OctDev oct) {
+                                                          OctDev oct, TexArgs tex) {
     const unsigned FULL = 0xffffffffu;
     const int tiles_x = (P.width + 7) >> 3;
     const unsigned total = (unsigned)tiles_x * (unsigned)((local_rows + 3) >> 2) * 32u;
     Ctx<T> C;
-    init_ctx(C, P, vol, nullptr, rp0, dist, mx, my, skip_on);
+    init_ctx(C, P, vol, nullptr, rp0, dist, mx, my, skip_on, tex);
     unsigned nsamp = 0, nshade = 0, nskip = 0, nhit = 0;
     RayState R;
     int px = 0, lr = 0;
@@ -714,13 +752,13 @@ __global__ void __launch_bounds__(128, GV ? VC_SHV_MINB : VC_SH_MINB) shade_kern
                                                        const uint8_t* __restrict__ dist, int mx, int my,
                                                        int skip_on, PixelSink sink,
                                                        unsigned long long* counters, FrameWork* work,
-                                                       const HitEntry* __restrict__ hits) {
+                                                       const HitEntry* __restrict__ hits, TexArgs tex) {
     const unsigned FULL = 0xffffffffu;
     const unsigned total = *(volatile unsigned*)&work->hits;
     __shared__ SharedLut s_lut;
     load_shared_lut(P, s_lut);
     Ctx<T> C;
-    init_ctx(C, P, vol, grad, rp0, dist, mx, my, skip_on);
+    init_ctx(C, P, vol, grad, rp0, dist, mx, my, skip_on, tex);
     C.lut = &s_lut;
     unsigned nsamp = 0, nshade = 0, nskip = 0, nhit = 0;
     RayState R;
@@ -820,12 +858,16 @@ static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     const long long tiles = (long long)((L.p->width + 7) / 8) * ((L.local_rows + 3) / 4);
     PixelSink sink{reinterpret_cast<uchar4*>(L.out), reinterpret_cast<uchar4* const*>(L.peers), L.npeers};
+    TexArgs tex{L.tex_value, L.tex_grad, L.tex_scale, 0.0f, 0.0f};
+    // v >= t_low <=> v >= RU(t_low) for a float v (and v <= t_high <=> v <= RD(t_high))
+    tex.lo = (float)L.p->t_low;
+    if ((double)tex.lo < L.p->t_low) tex.lo = std::nextafter(tex.lo, INFINITY);
+    tex.hi = (float)L.p->t_high;
+    if ((double)tex.hi > L.p->t_high) tex.hi = std::nextafter(tex.hi, -INFINITY);
     if (L.ev[0]) cudaEventRecord(L.ev[0], stream);
-    firsthit_kernel<T, OP, INTERP><<<persistent_blocks(firsthit_kernel<T, OP, INTERP>, (tiles + 3) / 4), 128, 0,
-                                     stream>>>(*L.p, vol, L.rp, L.occ, L.mx, L.my, L.skip_on, sink,
-                                               L.local_rows,
-                                               reinterpret_cast<unsigned long long*>(L.counters), fw, hits,
-                                               L.oct);
+    firsthit_kernel<T, INTERP><<<persistent_blocks(firsthit_kernel<T, INTERP>, (tiles + 3) / 4), 128, 0, stream>>>(
+        *L.p, vol, L.rp, L.occ, L.mx, L.my, L.skip_on, sink, L.local_rows,
+        reinterpret_cast<unsigned long long*>(L.counters), fw, hits, L.oct, tex);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (L.ev[1]) cudaEventRecord(L.ev[1], stream);
@@ -834,17 +876,18 @@ static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
     if (grad != nullptr)
         shade_kernel<T, OP, INTERP, true><<<persistent_blocks(shade_kernel<T, OP, INTERP, true>, (tiles + 3) / 4),
                                             128, 0, stream>>>(*L.p, vol, grad, L.rp, L.occ, L.mx, L.my,
-                                                              L.skip_on, sink, cnt, fw, hits);
+                                                              L.skip_on, sink, cnt, fw, hits, tex);
     else
         shade_kernel<T, OP, INTERP, false><<<persistent_blocks(shade_kernel<T, OP, INTERP, false>, (tiles + 3) / 4),
                                              128, 0, stream>>>(*L.p, vol, grad, L.rp, L.occ, L.mx, L.my,
-                                                               L.skip_on, sink, cnt, fw, hits);
+                                                               L.skip_on, sink, cnt, fw, hits, tex);
     if (L.ev[2]) cudaEventRecord(L.ev[2], stream);
     return cudaGetLastError();
 }
 
 template <typename T, int OP>
 static cudaError_t launch_op(const RenderLaunch& L, cudaStream_t s) {
+    if (L.p->sampler == VC_SAMPLER_TEXTURE) return launch_t<T, OP, VC_TEX>(L, s);  // trilinear (validated)
     switch (L.p->interp) {
         case VC_NEAREST: return launch_t<T, OP, VC_NEAREST>(L, s);
         case VC_LINEAR: return launch_t<T, OP, VC_LINEAR>(L, s);

@@ -48,6 +48,11 @@ struct RenderLaunch {
     void* hits;           // first-hit queue, >= local_rows * width entries
     cudaEvent_t ev[3];    // optional: recorded before stage 1, between, after stage 2
     OctDev oct;           // adaptive stepping (levels == 0 when unused)
+    // VC_SAMPLER_TEXTURE: tex3D objects over cudaArray copies of the grid
+    // (normalized-float read for integer grids, tex_scale undoes it) and of
+    // the float4 gradient volume (0 when grad == nullptr)
+    cudaTextureObject_t tex_value, tex_grad;
+    float tex_scale;
 };
 
 cudaError_t launch_raycast(const RenderLaunch& L, cudaStream_t s);

@@ -59,6 +59,8 @@ def main():
             sc, st = phantoms.scene_c3(vol, op=op, width=a.width, height=a.height, azimuth=float(i),
                                        mode=mode)
             st = replace(st, gradient_source=grad, use_octree="noskip" not in parts)
+            if "tex" in parts:  # hardware texture sampler
+                st = replace(st, sampler="texture")
             if "norefine" in parts:  # work accounting only: no bisection
                 st = replace(st, refine_iters=0)
             return render_params(vol, sc, st)

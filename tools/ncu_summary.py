@@ -25,6 +25,13 @@ METRICS = {
     "lts__t_sector_hit_rate.pct": "l2_hit_pct",
     "launch__registers_per_thread": "registers",
     "smsp__thread_inst_executed_per_inst_executed.ratio": "active_threads_per_warp",
+    # texture-path evidence (VC_SAMPLER_TEXTURE): texture data pipe and
+    # filter wavefronts, L1TEX throughput, L2 hit rate of texture traffic
+    "l1tex__data_pipe_tex_wavefronts.avg.pct_of_peak_sustained_elapsed": "l1tex_tex_pipe_pct",
+    "l1tex__f_wavefronts.avg.pct_of_peak_sustained_elapsed": "l1tex_filter_pct",
+    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed": "l1tex_lsu_pipe_pct",
+    "l1tex__throughput.avg.pct_of_peak_sustained_elapsed": "l1tex_throughput_pct",
+    "lts__average_t_sector_hit_rate_srcunit_tex_realtime.pct": "l2_hit_pct_tex_unit",
 }
 
 
@@ -55,8 +62,13 @@ def main():
         short = name.split("(")[0].replace("void ", "").split("<")[0]
         rec = {}
         for m, k in METRICS.items():
-            if m in head:
-                rec[k] = to_float(r[head.index(m)], units[head.index(m)])
+            # some columns carry a section prefix ("SM_A.TriageCompute.<metric>")
+            for col in [i for i, h in enumerate(head) if h == m] + \
+                    [i for i, h in enumerate(head) if h.endswith("." + m)]:
+                v = to_float(r[col], units[col])
+                if v is not None:
+                    rec[k] = v
+                    break
         per[short].append(rec)
     summary = {}
     for k, recs in per.items():
