@@ -58,8 +58,11 @@ struct vc_volume {
         void* work = nullptr;
         void* hits = nullptr;
         size_t hit_cap = 0;
+        cudaEvent_t done = nullptr;  // recorded after each render that used it
+        uint64_t stamp = 0;
     };
     std::unordered_map<cudaStream_t, StreamScratch> scratch;
+    uint64_t scratch_clock = 0;
     cudaStream_t host_stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::mutex mu;
@@ -193,6 +196,7 @@ void release(vc_volume* v) {
     for (auto& kv : v->scratch) {
         cudaFree(kv.second.work);
         cudaFree(kv.second.hits);
+        if (kv.second.done) cudaEventDestroy(kv.second.done);
     }
     if (v->host_stream) cudaStreamDestroy(v->host_stream);
     if (v->ev0) cudaEventDestroy(v->ev0);
@@ -393,8 +397,25 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
     L.out = d_rgba;
     L.local_rows = local_rows;
     L.counters = d_counters;
+    vc_volume::StreamScratch* scp = nullptr;
     {
+        // per-stream scratch, at most MAX_STREAM_SCRATCH streams: the least
+        // recently used one is released once its last render has finished
+        constexpr size_t MAX_STREAM_SCRATCH = 8;
+        if (v->scratch.find(s) == v->scratch.end() && v->scratch.size() >= MAX_STREAM_SCRATCH) {
+            auto old = v->scratch.begin();
+            for (auto it = v->scratch.begin(); it != v->scratch.end(); ++it)
+                if (it->second.stamp < old->second.stamp) old = it;
+            if (old->second.done) VC_CUDA(cudaEventSynchronize(old->second.done));
+            cudaFree(old->second.work);
+            cudaFree(old->second.hits);
+            if (old->second.done) cudaEventDestroy(old->second.done);
+            v->scratch.erase(old);
+        }
         auto& sc = v->scratch[s];
+        sc.stamp = ++v->scratch_clock;
+        if (!sc.done) VC_CUDA(cudaEventCreateWithFlags(&sc.done, cudaEventDisableTiming));
+        scp = &sc;
         const size_t need = (size_t)local_rows * p->width;
         if (sc.work == nullptr) VC_CUDA(cudaMalloc(&sc.work, vc::frame_work_bytes()));
         if (sc.hit_cap < need) {
@@ -441,6 +462,7 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
     if (local_rows == 0) return VC_OK;
     VC_CUDA(vc::launch_raycast(L, s));
     if (field) VC_CUDA(cudaEventRecord(field->last_use, s));
+    VC_CUDA(cudaEventRecord(scp->done, s));
     return VC_OK;
 }
 

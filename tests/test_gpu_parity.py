@@ -403,3 +403,40 @@ def test_render_frame_png_matches_render_frame():
     assert len(png) < fb.pixels[..., :3].nbytes / 2  # it compresses
     pkt = egress.frame_packet(7, png)
     assert int.from_bytes(pkt[:8], "big") == 7 and int.from_bytes(pkt[8:12], "big") == len(png)
+
+
+def test_many_streams_share_bounded_scratch():
+    """Renders on more streams than the library keeps scratch for (LRU of 8)
+    all produce the same frame."""
+    import ctypes
+
+    import torch
+
+    from paper_1609_01317_b200 import _native
+    from paper_1609_01317_b200.raycast import render_params
+
+    vol = phantoms.ct_phantom(64)
+    sc, st = phantoms.scene_c3(vol, width=96, height=64, azimuth=10.0)
+    want = vc.render_frame(vol, sc, st).pixels
+    dv = vc.device_volume(vol)
+    P = render_params(vol, sc, st)
+    L = _native.load()
+    outs = []
+    for _ in range(12):
+        s = torch.cuda.Stream()
+        out = torch.empty((64, 96, 4), dtype=torch.uint8, device="cuda")
+        _native.check(L.vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(out.data_ptr()), None,
+                                  ctypes.c_void_p(s.cuda_stream)))
+        outs.append((s, out))
+    for s, out in outs:
+        s.synchronize()
+        assert np.array_equal(out.cpu().numpy(), want)
+
+
+def test_render_sequence_reuses_resources():
+    vol = phantoms.ct_phantom(64)
+    frames = [phantoms.scene_c3(vol, width=96, height=64, azimuth=float(a)) for a in range(5)]
+    want = [vc.render_frame(vol, sc, st).pixels for sc, st in frames]
+    for _ in range(3):  # pooled streams / buffers across calls
+        got = [fb.pixels.copy() for fb in vc.render_sequence(vol, iter(frames))]
+        assert all(np.array_equal(a, b) for a, b in zip(got, want))
