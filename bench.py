@@ -215,6 +215,14 @@ def cpu_sample_fps(vol, frame, first_frame: int, target_s: float, threads: int):
                                 f"over frames {first_frame}..{f - 1} ({spent:.1f} s CPU wall)"
 
 
+def workload_config(args) -> dict:
+    """The workload keys both arms report (BASELINE.json configs[2], C3)."""
+    return {"workload": f"C3: {args.size}^3 uint16 3-D Shepp-Logan CT phantom, {args.width}x{args.height}, "
+                        f"{args.op}, {args.mode}, 1 deg/frame orbit",
+            "volume": f"{args.size}^3 uint16", "image": f"{args.width}x{args.height}", "operator": args.op,
+            "mode": args.mode}
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -224,7 +232,9 @@ def run_reference(args):
     from oracle import oracle
 
     oracle.build()
-    per_step = max(args.cpu_seconds / 4.0, 1.0)
+    # bounded: the whole --steps K --warmup W run stays around a minute of
+    # CPU wall time whatever K and W are (each step samples >= one band)
+    per_step = min(max(60.0 / max(args.warmup + args.steps, 1), 0.25), 3.0)
     fps_list = []
     for i in range(args.warmup + args.steps):
         fps, sample = cpu_sample_fps(vol, frame, i * 7, per_step, threads)
@@ -236,8 +246,9 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"C3: {args.size}^3 uint16 CT phantom, {args.width}x{args.height}, "
-                               f"{args.op}, {args.mode}, brute force (reference C port)"},
+        "config": {**workload_config(args),
+                   "implementation": "reference algorithm, brute force (C port of _kernels.render_tile, "
+                                     "bit-identical to the numba reference), all host threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"per step: {sample}; cpu: {lscpu_model()}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -551,10 +562,7 @@ def run_ours(args):
         "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"C3: {args.size}^3 uint16 3-D Shepp-Logan CT phantom, "
-                               f"{W}x{H}, {args.op}, {args.mode}, 1 deg/frame orbit",
-                   "volume": f"{args.size}^3 uint16", "image": f"{W}x{H}", "operator": args.op,
-                   "mode": args.mode, "gradient_source": args.grad,
+        "config": {**workload_config(args), "gradient_source": args.grad,
                    "empty_space_skipping": not args.no_skip,
                    "l2": "flushed between timed frames (256 MiB write, outside the event pair)",
                    "parallelism": f"image-plane row bands x{world}", "gather": gather_mode},
