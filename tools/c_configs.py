@@ -54,17 +54,19 @@ def main():
         gen_s = time.time() - t0
         dv = vc.device_volume(vol)
         res = {}
-        for grad in ("taps", "volume"):
+        variants = {"taps": dict(gradient_source="taps"), "volume": dict(gradient_source="volume"),
+                    "texture": dict(gradient_source="volume", sampler="texture")}
+        for grad, kw in variants.items():
             sc, st = scene(0)
             out = torch.empty((st.height, st.width, 4), dtype=torch.uint8, device="cuda")
             for i in range(3):
                 sc, st = scene(i)
-                P = render_params(vol, sc, replace(st, gradient_source=grad))
+                P = render_params(vol, sc, replace(st, **kw))
                 _native.check(L.vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(out.data_ptr()), None, sp))
             ts = []
             for i in range(a.frames):
                 sc, st = scene(10 + i)
-                P = render_params(vol, sc, replace(st, gradient_source=grad))
+                P = render_params(vol, sc, replace(st, **kw))
                 flush.zero_()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
@@ -79,8 +81,8 @@ def main():
         rows = (H // 2 - 4, H // 2 + 4)
         want, _ = oracle.render(vol.as_array(), vol.spacing, spec_of((sc, st)), rows=rows)
         par = {}
-        for grad in ("taps", "volume"):
-            fb = vc.render_frame(vol, sc, replace(st, gradient_source=grad))
+        for grad, kw in variants.items():
+            fb = vc.render_frame(vol, sc, replace(st, **kw))
             d = np.abs(fb.pixels[rows[0]:rows[1]].astype(int) - want[rows[0]:rows[1]].astype(int))
             par[grad] = int(d.max())
         print(json.dumps({"config": desc, "ms_per_frame": res, "fps": {k: 1000.0 / v for k, v in res.items()},
