@@ -185,6 +185,22 @@ def test_ct128_composited_vs_oracle(op):
     assert maxdiff(fb.pixels, want_px) <= 1
 
 
+@pytest.mark.parametrize("spacing", [(0.7, 0.9, 1.3), (1.0 / 3.0, 0.6, 2.5)])
+def test_anisotropic_spacing_vs_oracle(spacing):
+    """Non power-of-two spacing takes the reciprocal division path
+    (ddiv_rcp) for every ray position: still bit-exact, counts included."""
+    base = phantoms.ct_phantom(80)
+    vol = vc.Volume.from_array(base.as_array(), spacing=spacing)
+    for mode in ("surface", "composited"):
+        sc, st = phantoms.scene_c3(vol, width=160, height=90, azimuth=21.0, mode=mode)
+        want_px, want_count = _oracle_frame(vol, (sc, st))
+        fb = vc.render_frame(vol, sc, product_settings_from(st, use_octree=False))
+        assert np.array_equal(fb.pixels, want_px), f"max|d|={maxdiff(fb.pixels, want_px)}"
+        assert fb.sample_count == want_count
+        fb = vc.render_frame(vol, sc, product_settings_from(st, use_octree=True))
+        assert np.array_equal(fb.pixels, want_px)
+
+
 def test_marschner_lobb_c2_orbit_vs_oracle():
     vol = phantoms.marschner_lobb(64)
     for az in (0.0, 45.0, 200.0):

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--variants", default="volume,taps,volume+surface,volume+noskip")
+    ap.add_argument("--spacing", default="1,1,1", help="voxel spacing (non power-of-two: division path)")
     a = ap.parse_args()
 
     import torch
@@ -38,6 +39,9 @@ def main():
     from paper_1609_01317_b200.raycast import render_params
 
     vol = phantoms.ct_phantom(a.size)
+    sp = tuple(float(x) for x in a.spacing.split(","))
+    if sp != (1.0, 1.0, 1.0):
+        vol = vc.Volume.from_array(vol.as_array(), spacing=sp)
     dv = vc.device_volume(vol)
     L = _native.load(build_if_missing=False)
     out = torch.empty((a.height, a.width, 4), dtype=torch.uint8, device="cuda")
