@@ -166,7 +166,8 @@ VC_API int vc_device_count(int *out);
  * min/max grid used by empty-space skipping. */
 VC_API int vc_volume_create(int device, const void *h_data, int dtype, int nx, int ny, int nz,
                      const double spacing[3], vc_volume **out);
-/* same, from data already resident in HBM on `device` (copied). */
+/* same, from data already resident in HBM on `device` (copied): the
+ * device side of the raw-slice ingest (load_raw_slices, volume.py:197-242). */
 VC_API int vc_volume_create_device(int device, const void *d_data, int dtype, int nx, int ny, int nz,
                             const double spacing[3], vc_volume **out);
 VC_API int vc_volume_destroy(vc_volume *vol);
