@@ -67,6 +67,7 @@ class _Params(ctypes.Structure):
         ("nbounds", ctypes.POINTER(ctypes.c_int32)),
         ("sminmax", ctypes.POINTER(ctypes.c_double)),
         ("nchildren", ctypes.POINTER(ctypes.c_int32)),
+        ("use_octree", ctypes.c_int32),
     ]
 
 
@@ -395,9 +396,12 @@ def build_octree_flat(arr, min_block=4, max_depth=8):
     return nb, sm, ch
 
 
-def render(arr, spacing, spec: dict, threads=None, rows=None):
+def render(arr, spacing, spec: dict, threads=None, rows=None, octree: bool = False):
     """Brute-force frame (render_frame(..., use_octree=False)); with
     settings.use_adaptive the reference's adaptive stride over its octree.
+    octree=True honours settings.use_octree as the reference does: only the
+    merged octree segments are marched (collect_segments), which changes the
+    sample count (and, with use_adaptive, where the stride restarts).
 
     Returns (pixels (H,W,4) uint8, sample_count).  `rows` = (y0, y1)
     restricts the work to a row range (other rows stay zero)."""
@@ -405,6 +409,14 @@ def render(arr, spacing, spec: dict, threads=None, rows=None):
     P = make_params((nx, ny, nz), spacing, spec)
     s = spec.get("settings", {})
     keep = None
+    use_octree = bool(octree and s.get("use_octree", True))
+    if use_octree and not s.get("use_adaptive"):
+        nb, sm, ch = build_octree_flat(arr, s.get("octree_min_block", 4), s.get("octree_max_depth", 8))
+        keep = (nb, sm, ch)
+        P.nbounds = nb.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        P.sminmax = sm.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        P.nchildren = ch.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    P.use_octree = 1 if use_octree else 0
     if s.get("use_adaptive"):
         nb, sm, ch = build_octree_flat(arr, s.get("octree_min_block", 4), s.get("octree_max_depth", 8))
         keep = (nb, sm, ch)

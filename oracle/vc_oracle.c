@@ -70,6 +70,10 @@ typedef struct {
     const int32_t *nbounds;   /* N x 6 (lo xyz, hi xyz) */
     const double *sminmax;    /* N x 2 padded range */
     const int32_t *nchildren; /* N x 8, -1 padded */
+    /* use_octree (raycast.py:187): march only the merged t-segments of
+     * octree leaves whose padded range overlaps the window
+     * (collect_segments, _kernels.py:267-342) */
+    int32_t use_octree;
 } vco_params;
 
 /* _kernels.py:35-37 */
@@ -336,15 +340,78 @@ static int64_t adaptive_stride(const vco_vol *v, const vco_params *P, const doub
     return step_k;
 }
 
-/* _kernels.py:367-465, single segment [t_enter, t_exit], no octree
- * segments (the use_octree=False branch); adaptive stride when P (non-NULL)
- * asks for it. */
-static int first_hit_p(const vco_vol *v, const vco_params *P, const double sp[3], const double org[3],
-                       const double dirv[3], double t_enter, double t_exit, double coarse,
-                       double fine, double t_low, double t_high, int interp, int64_t *counter,
-                       double *t_hit, double *t_before, int *bracket) {
+#define VCO_SEG_CAP 4096   /* seg0 / seg1 of raycast.py:499 */
+#define VCO_STACK_CAP 512  /* stack of raycast.py:499 */
+
+/* _kernels.py:267-342: depth-first near-to-far walk emitting the merged
+ * t-intervals of leaves whose padded range overlaps [t_low, t_high]. */
+static int collect_segments(const vco_params *P, const double sp[3], const double org[3],
+                            const double dirv[3], double tray0, double tray1, double t_low,
+                            double t_high, int32_t *stack, double *seg0, double *seg1) {
+    int nseg = 0, top = 0;
+    stack[top++] = 0;
+    double child_t[8];
+    int32_t child_i[8];
+    while (top > 0) {
+        int32_t idx = stack[--top];
+        double a0, b0;
+        if (!node_interval(P, idx, sp, org, dirv, &a0, &b0)) continue;
+        if (a0 < tray0) a0 = tray0;
+        if (b0 > tray1) b0 = tray1;
+        if (b0 < a0) continue;
+        if (P->nchildren[idx * 8] < 0) {
+            if (P->sminmax[idx * 2] <= t_high && P->sminmax[idx * 2 + 1] >= t_low) {
+                if (nseg > 0 && a0 <= seg1[nseg - 1] + 1e-9) {
+                    if (b0 > seg1[nseg - 1]) seg1[nseg - 1] = b0;
+                } else if (nseg < VCO_SEG_CAP) {
+                    seg0[nseg] = a0;
+                    seg1[nseg] = b0;
+                    nseg++;
+                } else {
+                    seg1[nseg - 1] = b0;
+                }
+            }
+        } else {
+            int cnt = 0;
+            for (int c = 0; c < 8; c++) {
+                int32_t ci = P->nchildren[idx * 8 + c];
+                if (ci < 0) break;
+                double ca, cb;
+                if (!node_interval(P, ci, sp, org, dirv, &ca, &cb) || cb < tray0 || ca > tray1) continue;
+                child_t[cnt] = ca;
+                child_i[cnt] = ci;
+                cnt++;
+            }
+            /* insertion sort, farthest entry first so nearest pops first */
+            for (int a = 1; a < cnt; a++) {
+                double tv = child_t[a];
+                int32_t iv = child_i[a];
+                int b = a - 1;
+                while (b >= 0 && child_t[b] < tv) {
+                    child_t[b + 1] = child_t[b];
+                    child_i[b + 1] = child_i[b];
+                    b--;
+                }
+                child_t[b + 1] = tv;
+                child_i[b + 1] = iv;
+            }
+            for (int a = 0; a < cnt && top < VCO_STACK_CAP; a++) stack[top++] = child_i[a];
+        }
+    }
+    return nseg;
+}
+
+/* _kernels.py:367-465 over segments [seg0[i], seg1[i]] (one segment
+ * [t_enter, t_exit] when the octree is off); adaptive stride when P
+ * (non-NULL) asks for it. */
+static int first_hit_seg(const vco_vol *v, const vco_params *P, const double sp[3], const double org[3],
+                         const double dirv[3], double t_enter, double t_exit, const double *seg0,
+                         const double *seg1, int nseg, double coarse, double fine, double t_low,
+                         double t_high, int interp, int64_t *counter, double *t_hit, double *t_before,
+                         int *bracket) {
     int64_t k = 0;
-    double s0 = t_enter, s1 = t_exit;
+    for (int si = 0; si < nseg; si++) {
+    double s0 = seg0[si], s1 = seg1[si];
     if (s1 > t_exit) s1 = t_exit;
     int64_t kk = (int64_t)floor((s0 - t_enter) / coarse);
     if (kk > k) k = kk;
@@ -382,9 +449,19 @@ static int first_hit_p(const vco_vol *v, const vco_params *P, const double sp[3]
         if (P && P->use_adaptive) k += adaptive_stride(v, P, sp, org, dirv, p, k, t_enter, coarse);
         else k += 1;
     }
+    }
     *t_hit = *t_before = 0.0;
     *bracket = 0;
     return 0;
+}
+
+static int first_hit_p(const vco_vol *v, const vco_params *P, const double sp[3], const double org[3],
+                       const double dirv[3], double t_enter, double t_exit, double coarse,
+                       double fine, double t_low, double t_high, int interp, int64_t *counter,
+                       double *t_hit, double *t_before, int *bracket) {
+    const double s0 = t_enter, s1 = t_exit;
+    return first_hit_seg(v, P, sp, org, dirv, t_enter, t_exit, &s0, &s1, 1, coarse, fine, t_low, t_high,
+                         interp, counter, t_hit, t_before, bracket);
 }
 
 static int first_hit(const vco_vol *v, const double sp[3], const double org[3],
@@ -471,9 +548,16 @@ static void shade_sample(const vco_vol *v, const vco_params *P, const double org
     out[3] = m[3];
 }
 
-/* _kernels.py:582-797 for rows [y0, y1), octree off. */
+/* _kernels.py:582-797 for rows [y0, y1). */
 static void render_rows(const vco_vol *v, const vco_params *P, int y0, int y1, uint8_t *out,
                         int64_t *counter) {
+    int32_t *stack = NULL;
+    double *seg0 = NULL, *seg1 = NULL;
+    if (P->use_octree) {  /* per-band scratch, like raycast.py:499 */
+        stack = (int32_t *)malloc(VCO_STACK_CAP * sizeof(int32_t));
+        seg0 = (double *)malloc(VCO_SEG_CAP * sizeof(double));
+        seg1 = (double *)malloc(VCO_SEG_CAP * sizeof(double));
+    }
     uint8_t bgr = quant(P->bg[0]), bgg = quant(P->bg[1]), bgb = quant(P->bg[2]),
             bga = quant(P->bg[3]);
     const double *org = P->eye;
@@ -499,9 +583,18 @@ static void render_rows(const vco_vol *v, const vco_params *P, int y0, int y1, u
             double t_enter = iv[0], t_exit = iv[1];
             double t_in, t_before;
             int bracket;
-            int found = first_hit_p(v, P, P->spacing, org, dirv, t_enter, t_exit, P->coarse, P->fine,
+            int found;
+            if (P->use_octree) {
+                int nseg = collect_segments(P, P->spacing, org, dirv, t_enter, t_exit, P->t_low, P->t_high,
+                                            stack, seg0, seg1);
+                found = first_hit_seg(v, P, P->spacing, org, dirv, t_enter, t_exit, seg0, seg1, nseg,
+                                      P->coarse, P->fine, P->t_low, P->t_high, P->interp, counter, &t_in,
+                                      &t_before, &bracket);
+            } else {
+                found = first_hit_p(v, P, P->spacing, org, dirv, t_enter, t_exit, P->coarse, P->fine,
                                     P->t_low, P->t_high, P->interp, counter, &t_in, &t_before,
                                     &bracket);
+            }
             if (!found) {
                 o[0] = bgr; o[1] = bgg; o[2] = bgb; o[3] = bga;
                 continue;
@@ -545,6 +638,9 @@ static void render_rows(const vco_vol *v, const vco_params *P, int y0, int y1, u
             o[0] = quant(acc_r); o[1] = quant(acc_g); o[2] = quant(acc_b); o[3] = 255;
         }
     }
+    free(stack);
+    free(seg0);
+    free(seg1);
 }
 
 /* ---- exported entry points (ctypes) ---------------------------------- */

@@ -320,6 +320,13 @@ def test_adaptive_stride_vs_oracle(mode):
         assert fb.sample_count == want_count
         fb2 = vc.render_frame(vol, sc, replace(st2, gradient_source="volume"))
         assert maxdiff(fb2.pixels, want) <= 1
+        # use_octree=True as the reference runs it (segment restarts,
+        # restated in the oracle and pinned to the reference's counts): the
+        # same pixels; only the sample count differs
+        st3 = replace(st2, use_octree=True)
+        want3, _ = oracle.render(vol.as_array(), vol.spacing, spec_of((sc, st3)), octree=True)
+        fb3 = vc.render_frame(vol, sc, st3)
+        assert np.array_equal(fb3.pixels, want3)
 
 
 @pytest.mark.parametrize("shape", [(1, 8, 8), (8, 1, 8), (2, 2, 2), (3, 17, 5), (1, 1, 1)])

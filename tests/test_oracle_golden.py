@@ -22,6 +22,23 @@ def test_oracle_frame_matches_reference(golden, name):
         f"max |d| = {int(np.abs(got_px.astype(int) - want_px.astype(int)).max())}")
 
 
+def _octree_frames():
+    from tests.conftest import GOLDEN, Golden
+
+    return [e["name"] for e in Golden(GOLDEN).frames() if e["spec"].get("settings", {}).get("use_octree")]
+
+
+@pytest.mark.parametrize("name", _octree_frames())
+def test_oracle_octree_segments_match_reference_counts(golden, name):
+    """use_octree=True as the reference runs it (collect_segments,
+    _kernels.py:267-342, and the segment loop of first_hit): pixels AND
+    sample counts equal the reference's."""
+    arr, spacing, spec, want_px, want_count = golden.frame(name)
+    got_px, got_count = oracle.render(arr, spacing, spec, threads=4, octree=True)
+    assert np.array_equal(got_px, want_px)
+    assert got_count == want_count
+
+
 @pytest.mark.parametrize("interp", ["nearest", "linear", "trilinear"])
 def test_oracle_sample_matches_reference(golden, interp):
     got = oracle.sample(golden["points/noise16"], golden["points/pts"], interp)
