@@ -14,8 +14,10 @@ for rep in range(2):
     t = time.perf_counter()
     for f in frames: vc.render_frame(vol, *f, out=pinned)
     print("render_frame sync fps", len(frames) / (time.perf_counter() - t))
-for depth in (1, 2, 3):
-    for rep in range(3):
+for depth in (1, 2, 3, 4):
+    for fb in vc.render_sequence(vol, iter(frames[:8]), depth=depth):
+        pass
+    for rep in range(4):
         t = time.perf_counter(); ts = []
         for fb in vc.render_sequence(vol, iter(frames), depth=depth):
             ts.append(time.perf_counter())
