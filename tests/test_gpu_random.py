@@ -91,3 +91,21 @@ def test_random_scene_vs_oracle(volumes, i):
     assert np.array_equal(fb.pixels, want), "empty-space skipping changed pixels"
     fb = vc.render_frame(vol, sc, replace(st, gradient_source="volume"))
     assert int(np.abs(fb.pixels.astype(int) - want.astype(int)).max()) <= 1
+
+
+@pytest.mark.parametrize("i", range(32))
+def test_random_adaptive_scene_vs_oracle(volumes, i):
+    """use_adaptive on the same kind of random scenes (random stride factor,
+    detail epsilon, octree block size): bit-exact, counts included."""
+    rng = np.random.default_rng(5000 + i)
+    name = ["ct", "noise", "ml"][i % 3]
+    vol, sc, st = _scene(rng, volumes[name], name)
+    vmax = float(vol.as_array().max())
+    st = replace(st, use_adaptive=True, use_octree=False, adaptive_factor=int(rng.integers(1, 9)),
+                 detail_epsilon=None if rng.random() < 0.3 else float(rng.uniform(0.001, 0.3)) * vmax,
+                 octree_min_block=int(rng.choice([2, 4, 8])))
+    want, want_count = oracle.render(vol.as_array(), vol.spacing, spec_of((sc, st)), threads=8)
+    fb = vc.render_frame(vol, sc, st)
+    d = np.abs(fb.pixels.astype(int) - want.astype(int))
+    assert d.max() == 0, f"{int((d > 0).any(axis=2).sum())} px differ, max {int(d.max())}"
+    assert fb.sample_count == want_count
