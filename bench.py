@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-texture", action="store_true", help="skip the texture-sampler side measurement")
+    ap.add_argument("--timed-only", action="store_true",
+                    help="warm-up + timed frames only (for the ncu launch-list pass); reduced JSON line")
     ap.add_argument("--gather", default="peer", choices=("peer", "nccl"),
                     help="N>1: fused NVLink peer stores (validated) or NCCL all-gather")
     return ap.parse_args()
@@ -361,6 +363,23 @@ def run_ours(args):
     else:
         ms_total = ms_local
     fps = args.steps / (ms_total / 1000.0)
+    if args.timed_only:  # the profiling pass: only warm-up + timed frames ran
+        if peers is not None:
+            torch.distributed.barrier()
+            for pf in peers:
+                pf.close()
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world,
+                              "steps": args.steps, "warmup": args.warmup,
+                              "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+                              "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                              "data": "synthetic", "timed_only": True,
+                              "config": {**workload_config(args), "gradient_source": args.grad,
+                                         "gather": gather_mode},
+                              "gpu_launches": 2 * args.steps, "clocks": clk.summary()}), flush=True)
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
 
     # brute-force work counts of the timed frames (our skip-off counts equal
     # the reference's sample counts, tests/test_gpu_parity.py), untimed; per
