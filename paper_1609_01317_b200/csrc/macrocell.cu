@@ -70,10 +70,8 @@ __global__ void __launch_bounds__(128) macrocell_minmax_kernel(const T* __restri
 }
 
 // occupancy of the window [lo, hi]: 0 = may hold an in-window sample,
-// DIST_CAP = empty.  Empty cells start at the cap, not at infinity: after
-// DIST_PASSES relaxation passes every cell within DIST_PASSES of an
-// occupied one holds its exact distance, and every other cell keeps
-// DIST_CAP = DIST_PASSES + 1, a valid lower bound of its distance.
+// DIST_CAP = empty.  Distances are capped at DIST_CAP = DIST_PASSES + 1
+// (the largest jump, in macrocells), a valid lower bound beyond it.
 constexpr uint8_t DIST_CAP = DIST_PASSES + 1;
 
 __global__ void occupancy_kernel(const float2* __restrict__ mm, int count, double lo, double hi,
@@ -84,32 +82,28 @@ __global__ void occupancy_kernel(const float2* __restrict__ mm, int count, doubl
     }
 }
 
-// One relaxation pass of the Chebyshev (L-infinity) distance transform of
-// the occupancy over the 26-neighbourhood.  Macrocells outside the grid
-// hold no in-range sample and count as empty.  Shortest 26-neighbour paths
-// have exactly the Chebyshev length, so dist[m] = d >= 1 guarantees that
-// every macrocell within Chebyshev distance d - 1 of m is empty.
-__global__ void chebyshev_pass_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int mx,
-                                      int my, int mz) {
+// Chebyshev (L-infinity) distance transform of the occupancy, capped at
+// DIST_CAP, in three separable 1-D passes:
+//   D(c) = min_c' max(|dx|, |dy|, |dz|) = min_dz max(|dz|, min_dy max(|dy|,
+//          min_dx max(|dx|, occ(c + d))))
+// each pass over a window of +-DIST_CAP cells along one axis (outside the
+// grid counts as empty).  dist[m] = d >= 1 guarantees that every macrocell
+// within Chebyshev distance d - 1 of m is empty.  The result equals
+// DIST_PASSES relaxation passes over the 26-neighbourhood (exact up to
+// DIST_PASSES, DIST_CAP beyond) in 3 launches instead of 16.
+__global__ void chebyshev_axis_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int mx,
+                                      int my, int mz, int axis) {
     const int count = mx * my * mz;
+    const int n = axis == 0 ? mx : (axis == 1 ? my : mz);
+    const int stride = axis == 0 ? 1 : (axis == 1 ? mx : mx * my);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
-        const int x = i % mx, y = (i / mx) % my, z = i / (mx * my);
+        const int c = axis == 0 ? i % mx : (axis == 1 ? (i / mx) % my : i / (mx * my));
         int best = in[i];
-        if (best != 0) {
-            for (int dz = -1; dz <= 1; dz++) {
-                const int zz = z + dz;
-                if (zz < 0 || zz >= mz) continue;
-                for (int dy = -1; dy <= 1; dy++) {
-                    const int yy = y + dy;
-                    if (yy < 0 || yy >= my) continue;
-                    for (int dx = -1; dx <= 1; dx++) {
-                        const int xx = x + dx;
-                        if (xx < 0 || xx >= mx) continue;
-                        const int v = in[(zz * my + yy) * mx + xx] + 1;
-                        if (v < best) best = v;
-                    }
-                }
-            }
+        for (int d = 1; d < best; d++) {  // max(d, .) >= d: nothing at distance >= best can improve
+            int v = DIST_CAP;
+            if (c - d >= 0) v = min(v, (int)in[i - d * stride]);
+            if (c + d < n) v = min(v, (int)in[i + d * stride]);
+            best = min(best, max(d, v));
         }
         out[i] = (uint8_t)best;
     }
@@ -141,13 +135,10 @@ cudaError_t launch_occupancy(const float2* mm, int mx, int my, int mz, double lo
     int blocks = (count + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
-    occupancy_kernel<<<blocks, 256, 0, s>>>(mm, count, lo, hi, dist);
-    // distances up to DIST_PASSES + 1 macrocells (8 voxels each); an even
-    // pass count leaves the result in `dist`
-    for (int p = 0; p < DIST_PASSES; p += 2) {
-        chebyshev_pass_kernel<<<blocks, 256, 0, s>>>(dist, scratch, mx, my, mz);
-        chebyshev_pass_kernel<<<blocks, 256, 0, s>>>(scratch, dist, mx, my, mz);
-    }
+    occupancy_kernel<<<blocks, 256, 0, s>>>(mm, count, lo, hi, scratch);
+    chebyshev_axis_kernel<<<blocks, 256, 0, s>>>(scratch, dist, mx, my, mz, 0);
+    chebyshev_axis_kernel<<<blocks, 256, 0, s>>>(dist, scratch, mx, my, mz, 1);
+    chebyshev_axis_kernel<<<blocks, 256, 0, s>>>(scratch, dist, mx, my, mz, 2);
     return cudaGetLastError();
 }
 
