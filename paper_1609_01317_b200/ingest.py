@@ -7,7 +7,8 @@ what it needs per call; its service rebuilds the octree per dataset switch
 (same validation and errors) but overlaps the three costs of bringing a
 dataset up on the B200:
 
-  disk -> pinned host chunk (a reader thread, file.readinto, no extra copy)
+  disk -> pinned host chunk (a reader thread and a small pool reading the
+                              chunk's slices concurrently, file.readinto)
   pinned chunk -> HBM        (cudaMemcpyAsync on a side stream, chunk i while
                               chunk i+1 is read)
   HBM-side work              (byte swap for big-endian files, the 12-bit
@@ -33,7 +34,7 @@ from .volume import MAX_12BIT, DeviceVolume, Volume, _slice_path, adopt_device_v
 def load_raw_slices_device(pattern: str, slice_width: int, slice_height: int, slice_count: int,
                            endianness: str = "little", *, first_index: int = 0,
                            strict_12bit: bool = False, spacing=(1.0, 1.0, 1.0), device: int = 0,
-                           prepass_ops=(), chunk_slices: int = 16) -> Volume:
+                           prepass_ops=(), chunk_slices: int = 16, readers: int = 4) -> Volume:
     """load_raw_slices (volume.py:197-242 of the reference: same arguments,
     checks and errors) that leaves the volume resident on `device`, with the
     gradient pre-pass of each operator in `prepass_ops` already built."""
@@ -65,25 +66,34 @@ def load_raw_slices_device(pattern: str, slice_width: int, slice_height: int, sl
     slot_free = [threading.Semaphore(1), threading.Semaphore(1)]
     stop = threading.Event()
 
+    def read_slice(k, view, c0):
+        path = _slice_path(pattern, first_index + k)
+        with open(path, "rb") as fh:
+            size = os.fstat(fh.fileno()).st_size
+            if size != per:
+                raise OSError(f"{path}: expected {per} bytes "
+                              f"({slice_width}x{slice_height} uint16), found {size}")
+            got = fh.readinto(memoryview(view[(k - c0) * per:(k - c0 + 1) * per]))
+        if got != per:
+            raise OSError(f"{path}: short read ({got} of {per} bytes)")
+
     def reader():
+        from concurrent.futures import ThreadPoolExecutor
+
         try:
-            for c0 in range(0, N, chunk):
-                slot = (c0 // chunk) % 2
-                slot_free[slot].acquire()
-                if stop.is_set():
-                    return
-                view = ring[slot].numpy().view(np.uint8).reshape(-1)
-                for k in range(c0, min(c0 + chunk, N)):
-                    path = _slice_path(pattern, first_index + k)
-                    with open(path, "rb") as fh:
-                        size = os.fstat(fh.fileno()).st_size
-                        if size != per:
-                            raise OSError(f"{path}: expected {per} bytes "
-                                          f"({slice_width}x{slice_height} uint16), found {size}")
-                        got = fh.readinto(memoryview(view[(k - c0) * per:(k - c0 + 1) * per]))
-                    if got != per:
-                        raise OSError(f"{path}: short read ({got} of {per} bytes)")
-                filled.put((c0, slot, None))
+            # the slices of a chunk are read concurrently (file reads release
+            # the GIL); errors surface in slice order, like the sequential loader
+            with ThreadPoolExecutor(max_workers=max(1, min(readers, chunk))) as pool:
+                for c0 in range(0, N, chunk):
+                    slot = (c0 // chunk) % 2
+                    slot_free[slot].acquire()
+                    if stop.is_set():
+                        return
+                    view = ring[slot].numpy().view(np.uint8).reshape(-1)
+                    futs = [pool.submit(read_slice, k, view, c0) for k in range(c0, min(c0 + chunk, N))]
+                    for f in futs:
+                        f.result()
+                    filled.put((c0, slot, None))
         except BaseException as exc:  # re-raised in the caller's thread
             filled.put((None, None, exc))
 
