@@ -270,12 +270,21 @@ def run_ours(args):
     from paper_1609_01317_b200.raycast import render_params, sample_count_of
 
     world, rank, local = dist_env()
+    # VC_BENCH_DIST_BACKEND=gloo VC_BENCH_DEVICE=0: run the N>1 control flow
+    # (peer-frame validation, gathers, max-over-ranks timing, e2e) with all
+    # ranks on one GPU -- a functional check, not a scaling measurement
+    backend = os.environ.get("VC_BENCH_DIST_BACKEND", "nccl")
+    if "VC_BENCH_DEVICE" in os.environ:
+        local = int(os.environ["VC_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     dev = local
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     vol, frame = build_workload(args)
     L = _native.load(build_if_missing=False)
     dv = vc.device_volume(vol, dev)
@@ -622,6 +631,8 @@ def run_ours(args):
                              "of the work counters)",
         "clocks": clk.summary(),
         "parity": parity,
+        **({"functional_check_only": f"{backend} backend, ranks sharing one GPU"}
+           if backend != "nccl" and world > 1 else {}),
         "exact_fp64_path": exact,
         "texture_path": texture,
         "wall_s_timed_region": t_wall,

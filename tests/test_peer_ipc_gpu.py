@@ -84,3 +84,27 @@ def test_peer_store_gather_across_processes(tmp_path, world):
     for r in range(world):
         got = np.load(out + f"_rank{r}.npy")
         assert np.array_equal(got, ref), f"rank {r} frame differs"
+
+
+@pytest.mark.gpu
+def test_bench_multi_rank_flow_on_one_gpu(tmp_path):
+    """bench.py's N > 1 control flow end to end (peer-frame set-up and its
+    validation against the all-gather, max-over-ranks timing, the
+    distributed e2e path, one JSON line from rank 0) with two ranks on the
+    one GPU over gloo -- a functional check of the path the scaling run
+    takes, not a measurement."""
+    import json
+
+    env = dict(os.environ, VC_BENCH_DIST_BACKEND="gloo", VC_BENCH_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(ROOT / "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-texture", "--size", "256"]
+    p = subprocess.run(cmd, env=env, cwd=str(ROOT), capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["config"]["gather"].startswith("peer (fused NVLink stores, validated")
+    assert d["e2e"]["value"] > 0
+    assert d["parity"]["max_abs_diff_vs_fp64_taps_bruteforce"] <= 1
