@@ -87,9 +87,12 @@ __device__ __forceinline__ double skip_to(double t, double k, double base, const
     for (int a = 0; a < 3; a++) {
         const int lo = (c[a] >> MC_SHIFT) << MC_SHIFT;
         const double ib = sk.ib[a];
-        // box face in voxel units (exact int -> double on the FP64 pipe, no XU)
-        if (ib > 0.0) dt = fmin(dt, (u2d((uint32_t)(lo + (1 << MC_SHIFT) + r)) - EPS - p[a]) * ib);
-        else if (ib < 0.0) dt = fmin(dt, (biased2d((uint32_t)(lo - r) + 0x80000000u) + EPS - p[a]) * ib);
+        // the box face ahead, in voxel units (branch-free: selects, one exact
+        // int -> double on the FP64 pipe); a zero direction adds no limit
+        const bool up = ib > 0.0;
+        const int face = up ? lo + (1 << MC_SHIFT) + r : lo - r;
+        const double cand = (biased2d((uint32_t)face + 0x80000000u) + (up ? -EPS : EPS) - p[a]) * ib;
+        dt = ib != 0.0 ? fmin(dt, cand) : dt;
     }
     double kn = k + 1.0;
     if (dt > 0.0) {
