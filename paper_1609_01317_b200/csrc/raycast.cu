@@ -394,11 +394,19 @@ __device__ __forceinline__ bool start_ray(Ctx<T>& C, const vc_render_params& P, 
 // Adaptive stride after an out-of-window first-hit sample at p with lattice
 // index k (_kernels.py:437-463): leaf_for_point (:345-364) over the level
 // grid, then _node_interval (:227-264) of the leaf when its padded range is
-// below detail_eps.  Same float64 operations as the reference.
-template <typename T>
-__device__ __forceinline__ double adaptive_stride(const OctDev& o, const Ctx<T>& C, const vc_render_params& P,
-                                                  const double p[3], double k, double t_enter) {
-    const int n3[3] = {C.v.nx, C.v.ny, C.v.nz};
+// below detail_eps.  Same float64 operations as the reference.  Out of line
+// with by-value arguments: the mode is rare and inlining it into the march
+// loop cost every other mode code size and registers.
+struct StrideArgs {
+    int nx, ny, nz, adapt_jump;
+    double o[3], d[3], s[3];
+    double detail_eps, coarse;
+};
+
+__device__ __noinline__ double adaptive_stride(const OctDev o, const StrideArgs A, double p0, double p1,
+                                               double p2, double k, double t_enter) {
+    const double p[3] = {p0, p1, p2};
+    const int n3[3] = {A.nx, A.ny, A.nz};
     int ic[3];
 #pragma unroll
     for (int a = 0; a < 3; a++) {
@@ -407,29 +415,29 @@ __device__ __forceinline__ double adaptive_stride(const OctDev& o, const Ctx<T>&
         i = i < 0 ? 0 : (i > n3[a] - 1 ? n3[a] - 1 : i);
         ic[a] = i;
     }
-    const int stride_map = C.v.nx + C.v.ny + C.v.nz;
+    const int stride_map = A.nx + A.ny + A.nz;
     int L = 0, b[3] = {0, 0, 0};
     long long leaf = 0;
     for (L = 0; L < o.levels; L++) {
         const int* m = o.amap + (size_t)L * stride_map;
         b[0] = __ldg(m + ic[0]);
-        b[1] = __ldg(m + C.v.nx + ic[1]);
-        b[2] = __ldg(m + C.v.nx + C.v.ny + ic[2]);
+        b[1] = __ldg(m + A.nx + ic[1]);
+        b[2] = __ldg(m + A.nx + A.ny + ic[2]);
         leaf = __ldg(o.box_off + L) +
                ((long long)b[2] * __ldg(o.dims + 3 * L + 1) + b[1]) * __ldg(o.dims + 3 * L + 0) + b[0];
         if (__ldg(o.state + leaf) == 2) break;
     }
     if (L == o.levels) return 1.0;  // unreachable for a well-formed tree
     const double smin = __ldg(o.srange + 2 * leaf), smax = __ldg(o.srange + 2 * leaf + 1);
-    if (!(dsub(smax, smin) < P.detail_eps)) return 1.0;
+    if (!(dsub(smax, smin) < A.detail_eps)) return 1.0;
     // _node_interval of the leaf box
     double tmin = -1e300, tmax = 1e300;
 #pragma unroll
     for (int a = 0; a < 3; a++) {
         const int* iv = o.ivl + __ldg(o.ivl_off + 3 * L + a) + 2 * b[a];
-        const double lo = dmul((double)__ldg(iv), C.rp.s[a]);
-        const double hi = dmul((double)__ldg(iv + 1), C.rp.s[a]);
-        const double ov = C.rp.o[a], d = C.rp.d[a];
+        const double lo = dmul((double)__ldg(iv), A.s[a]);
+        const double hi = dmul((double)__ldg(iv + 1), A.s[a]);
+        const double ov = A.o[a], d = A.d[a];
         if (d == 0.0) {
             if (ov < lo || ov > hi) return 1.0;
         } else {
@@ -445,8 +453,8 @@ __device__ __forceinline__ double adaptive_stride(const OctDev& o, const Ctx<T>&
         }
     }
     if (tmin > tmax) return 1.0;
-    double step = (double)P.adapt_jump;
-    const double kex = floor(ddiv(dsub(tmax, t_enter), P.coarse)) + 1.0;
+    double step = (double)A.adapt_jump;
+    const double kex = floor(ddiv(dsub(tmax, t_enter), A.coarse)) + 1.0;
     if (dsub(kex, k) < step) step = dsub(kex, k);
     if (step < 1.0) step = 1.0;
     return step;
@@ -468,7 +476,20 @@ __device__ __forceinline__ void march_step(const Ctx<T>& C, const vc_render_para
     if (w < 0) return;
     nsamp++;
     if (oct != nullptr && !w) {  // first-hit stage, adaptive mode
-        R.k += adaptive_stride(*oct, C, P, p, R.k, R.t_enter);
+        StrideArgs A;
+        A.nx = C.v.nx;
+        A.ny = C.v.ny;
+        A.nz = C.v.nz;
+        A.adapt_jump = P.adapt_jump;
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            A.o[a] = C.rp.o[a];
+            A.d[a] = C.rp.d[a];
+            A.s[a] = C.rp.s[a];
+        }
+        A.detail_eps = P.detail_eps;
+        A.coarse = P.coarse;
+        R.k += adaptive_stride(*oct, A, p[0], p[1], p[2], R.k, R.t_enter);
         return;
     }
     R.k += 1.0;
