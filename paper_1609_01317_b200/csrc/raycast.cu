@@ -683,6 +683,7 @@ __device__ __forceinline__ unsigned warp_ticket(unsigned* ctr, bool want) {
 #ifndef VC_FH_MINB
 #define VC_FH_MINB 8
 #endif
+
 #ifndef VC_SH_MINB
 #define VC_SH_MINB 5
 #endif
@@ -734,8 +735,10 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
             const bool need = active && !R.found && !R.exhausted;
             const unsigned mneed = __ballot_sync(FULL, need);
             if (mneed == 0) break;
-            const unsigned mact = __ballot_sync(FULL, active);
-            if (__popc(mact & ~mneed) * READY_DEN >= __popc(mact) * VC_FH_READY) break;
+            if (VC_FH_READY < READY_DEN) {  // (at READY_DEN the mneed == 0 exit above is the rule)
+                const unsigned mact = __ballot_sync(FULL, active);
+                if (__popc(mact & ~mneed) * READY_DEN >= __popc(mact) * VC_FH_READY) break;
+            }
             if (need) march_step<T, INTERP>(C, P, R, nsamp, nskip, P.use_adaptive ? &oct : nullptr);
         }
         const bool hit = active && R.found;
