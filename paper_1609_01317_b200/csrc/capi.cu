@@ -103,6 +103,13 @@ vc::RayPos make_raypos(const vc_volume* v) {
         pow2 = pow2 && is_pow2(v->spacing[a]);
     }
     rp.pow2 = pow2;
+    // ddiv_rcp needs rs = RN(1/s) (1.0 / s above) and no all-ones significand
+    rp.rcp = true;
+    for (int a = 0; a < 3; a++) {
+        uint64_t bits;
+        memcpy(&bits, &v->spacing[a], sizeof(bits));
+        if ((bits & 0xFFFFFFFFFFFFFull) == 0xFFFFFFFFFFFFFull) rp.rcp = false;
+    }
     return rp;
 }
 

@@ -271,9 +271,9 @@ __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_pa
     const double wy = dadd(r.o[1], dmul(t, r.d[1]));
     const double wz = dadd(r.o[2], dmul(t, r.d[2]));
     double p[3];
-    p[0] = dsub(r.pow2 ? dmul(wx, r.rs[0]) : ddiv(wx, r.s[0]), 0.5);
-    p[1] = dsub(r.pow2 ? dmul(wy, r.rs[1]) : ddiv(wy, r.s[1]), 0.5);
-    p[2] = dsub(r.pow2 ? dmul(wz, r.rs[2]) : ddiv(wz, r.s[2]), 0.5);
+    p[0] = dsub(r.vox(wx, 0), 0.5);
+    p[1] = dsub(r.vox(wy, 1), 0.5);
+    p[2] = dsub(r.vox(wz, 2), 0.5);
     double val, illum = 0.0;
     const bool interior = p[0] >= 1.0 && p[0] <= dsub(C.v.mx, 1.0) && p[1] >= 1.0 &&
                           p[1] <= dsub(C.v.my, 1.0) && p[2] >= 1.0 && p[2] <= dsub(C.v.mz, 1.0);

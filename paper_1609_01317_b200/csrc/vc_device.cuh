@@ -41,6 +41,19 @@ __device__ __forceinline__ double ddiv(double a, double b) {
     return __ddiv_rn(a, b);
 }
 
+// a / b, correctly rounded, from y = RN(1/b) (Markstein: q = RN(a y) is
+// within 1 ulp of a/b; the fma residual and one fma correction give
+// RN(a/b)).  Three FP64 instructions instead of the ~40 of __ddiv_rn.
+// Used for b = voxel spacing (per-volume constant y = 1.0 / s from the
+// host); spacings with an all-ones significand, which the classic statement
+// of the theorem excludes, take ddiv_cold instead (RayPos::rcp).
+__device__ __forceinline__ double ddiv_rcp(double a, double b, double y) {
+    const double q = __dmul_rn(a, y);
+    const double r = __fma_rn(-q, b, a);
+    return __fma_rn(r, y, q);
+}
+static __device__ __noinline__ double ddiv_cold(double a, double b) { return ddiv(a, b); }
+
 // _kernels.py:35-37
 __device__ __forceinline__ double lerp(double f0, double f1, double t) {
     return dadd(f0, dmul(dsub(f1, f0), t));
@@ -559,15 +572,18 @@ __device__ __forceinline__ bool box_interval(const double o[3], const double d[3
 // When every spacing is a power of two the division is exact as a
 // multiply by the (exact) reciprocal, so UNIT/POW2 spacing takes the fast
 // form without changing a bit.
+// Other spacings divide through the correctly rounded reciprocal rs
+// (ddiv_rcp, exact).
 struct RayPos {
     double o[3], d[3], s[3], rs[3];
     bool pow2;
+    bool rcp;  // every rs[a] usable by ddiv_rcp (host: make_raypos)
+    __device__ __forceinline__ double vox(double w, int a) const {
+        return pow2 ? dmul(w, rs[a]) : (rcp ? ddiv_rcp(w, s[a], rs[a]) : ddiv_cold(w, s[a]));
+    }
     __device__ __forceinline__ void at(double t, double p[3]) const {
 #pragma unroll
-        for (int a = 0; a < 3; a++) {
-            const double w = dadd(o[a], dmul(t, d[a]));
-            p[a] = dsub(pow2 ? dmul(w, rs[a]) : ddiv(w, s[a]), 0.5);
-        }
+        for (int a = 0; a < 3; a++) p[a] = dsub(vox(dadd(o[a], dmul(t, d[a])), a), 0.5);
     }
 };
 
