@@ -61,6 +61,7 @@ struct Ctx {
     RayPos rp;
     Skip sk;
     TexArgs tx;
+    double rmu;                       // rcp_for(mu_water): the HU division
     const SharedLut* lut;             // shade stage: transfer breakpoints in shared memory
 };
 
@@ -322,7 +323,7 @@ __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_pa
         if (ln > 0.0) illum = ddiv(dadd(dadd(dmul(lx, snx), dmul(ly, sny)), dmul(lz, snz)), ln);
     }
     illum = clamp01(illum);
-    const double hu = dmul(ddiv(dsub(val, P.mu_water), P.mu_water), 1000.0);
+    const double hu = dmul(div_rcp(dsub(val, P.mu_water), P.mu_water, C.rmu), 1000.0);
     double m[4];
     lut_eval(*C.lut, hu, m);
     Rgba out;
@@ -628,6 +629,7 @@ __device__ __forceinline__ void init_ctx(Ctx<T>& C, const vc_render_params& P, c
                                          int my, int skip_on, const TexArgs& tex) {
     C.v = vol;
     C.tx = tex;
+    C.rmu = rcp_for(P.mu_water);
     C.grad = grad;
     C.rp = rp0;
 #pragma unroll

@@ -53,6 +53,16 @@ __device__ __forceinline__ double ddiv_rcp(double a, double b, double y) {
     return __fma_rn(r, y, q);
 }
 static __device__ __noinline__ double ddiv_cold(double a, double b) { return ddiv(a, b); }
+// y = rcp_for(b): RN(1/b), or 0 when b is not a positive finite value with
+// a usable significand; div_rcp(a, b, y) = RN(a / b) either way
+__device__ __forceinline__ double rcp_for(double b) {
+    const bool ok = b > 0.0 && b < 1e300 &&
+                    (__double_as_longlong(b) & 0xFFFFFFFFFFFFFLL) != 0xFFFFFFFFFFFFFLL;
+    return ok ? __drcp_rn(b) : 0.0;
+}
+__device__ __forceinline__ double div_rcp(double a, double b, double y) {
+    return y != 0.0 ? ddiv_rcp(a, b, y) : ddiv_cold(a, b);
+}
 
 // _kernels.py:35-37
 __device__ __forceinline__ double lerp(double f0, double f1, double t) {
@@ -535,9 +545,10 @@ __device__ __forceinline__ void normalize3(const double g[3], double u[3]) {
         u[0] = u[1] = u[2] = 0.0;
         return;
     }
-    u[0] = ddiv(g[0], n);
-    u[1] = ddiv(g[1], n);
-    u[2] = ddiv(g[2], n);
+    const double y = rcp_for(n);
+    u[0] = div_rcp(g[0], n, y);
+    u[1] = div_rcp(g[1], n, y);
+    u[2] = div_rcp(g[2], n, y);
 }
 
 // _kernels.py:188-224 (slab_interval + box_interval)
@@ -619,6 +630,7 @@ __device__ __forceinline__ void lut_eval(const vc_render_params& P, double hu, d
 struct SharedLut {
     double hu[VC_MAX_LUT];
     double rgba[VC_MAX_LUT][4];
+    double rw[VC_MAX_LUT];  // rcp_for(hu[i+1] - hu[i]) for the segment division
     int n;
 };
 
@@ -639,7 +651,7 @@ __device__ __forceinline__ void lut_eval(const SharedLut& L, double hu, double o
     }
     i = 0;
     while (i + 1 < n - 1 && L.hu[i + 1] <= hu) i++;
-    const double t = ddiv(dsub(hu, L.hu[i]), dsub(L.hu[i + 1], L.hu[i]));
+    const double t = div_rcp(dsub(hu, L.hu[i]), dsub(L.hu[i + 1], L.hu[i]), L.rw[i]);
 #pragma unroll
     for (int c = 0; c < 4; c++) out[c] = lerp(L.rgba[i][c], L.rgba[i + 1][c], t);
 }
@@ -649,6 +661,7 @@ __device__ __forceinline__ void load_shared_lut(const vc_render_params& P, Share
         L.hu[k] = P.lut_hu[k];
 #pragma unroll
         for (int c = 0; c < 4; c++) L.rgba[k][c] = P.lut_rgba[k][c];
+        L.rw[k] = k + 1 < P.lut_n ? rcp_for(dsub(P.lut_hu[k + 1], P.lut_hu[k])) : 0.0;
     }
     if (threadIdx.x == 0) L.n = P.lut_n;
     __syncthreads();
