@@ -373,10 +373,12 @@ __device__ __forceinline__ bool start_ray(Ctx<T>& C, const vc_render_params& P, 
 #pragma unroll
     for (int a = 0; a < 3; a++) d[a] = dadd(dadd(P.forward[a], dmul(uw, P.right[a])), dmul(vh, P.up[a]));
     const double dn = __dsqrt_rn(dadd(dadd(dmul(d[0], d[0]), dmul(d[1], d[1])), dmul(d[2], d[2])));
+    const double ydn = rcp_for(dn);
 #pragma unroll
     for (int a = 0; a < 3; a++) {
-        C.rp.d[a] = ddiv(d[a], dn);
-        C.sk.ib[a] = C.rp.d[a] == 0.0 ? 0.0 : C.rp.s[a] / C.rp.d[a];
+        C.rp.d[a] = div_rcp(d[a], dn, ydn);
+        // skip_to's reciprocal speed: only conservativeness matters (EPS margins)
+        C.sk.ib[a] = C.rp.d[a] == 0.0 ? 0.0 : dmul(C.rp.s[a], __drcp_rn(C.rp.d[a]));
     }
     double t_enter, t_exit;
     if (!box_interval(C.rp.o, C.rp.d, P.clip_lo, P.clip_hi, t_enter, t_exit)) return false;

@@ -560,7 +560,7 @@ __device__ __forceinline__ bool box_interval(const double o[3], const double d[3
         if (d[a] == 0.0) {
             if (o[a] < lo[a] || o[a] > hi[a]) return false;
         } else {
-            const double inv = ddiv(1.0, d[a]);
+            const double inv = __drcp_rn(d[a]);  // = RN(1.0 / d), the reference's value
             double ta = dmul(dsub(lo[a], o[a]), inv);
             double tb = dmul(dsub(hi[a], o[a]), inv);
             if (ta > tb) {
