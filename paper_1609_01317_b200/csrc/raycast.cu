@@ -366,8 +366,9 @@ __device__ __forceinline__ int image_row(const vc_render_params& P, int lr) {
 template <typename T>
 __device__ __forceinline__ bool start_ray(Ctx<T>& C, const vc_render_params& P, int px, int py,
                                           RayState& R) {
-    const double v_ndc = dsub(1.0, ddiv(dmul(2.0, dadd((double)py, 0.5)), (double)P.height));
-    const double u_ndc = dsub(ddiv(dmul(2.0, dadd((double)px, 0.5)), (double)P.width), 1.0);
+    const double H = (double)P.height, W = (double)P.width;  // integers: never an all-ones significand
+    const double v_ndc = dsub(1.0, ddiv_rcp(dmul(2.0, dadd((double)py, 0.5)), H, __drcp_rn(H)));
+    const double u_ndc = dsub(ddiv_rcp(dmul(2.0, dadd((double)px, 0.5)), W, __drcp_rn(W)), 1.0);
     const double uw = dmul(u_ndc, P.half_w), vh = dmul(v_ndc, P.half_h);
     double d[3];
 #pragma unroll
