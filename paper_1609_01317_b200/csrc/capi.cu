@@ -4,8 +4,8 @@
 // A vc_volume owns, on one device:
 //   * the voxel grid (immutable after create; the reference Volume is frozen,
 //     volume.py:47, :71-72)
-//   * the 8^3 macrocell min/max grid (built once) and the occupancy bytes of
-//     the last threshold window (rebuilt only when the window changes)
+//   * the 4^3 macrocell min/max grid (built once) and the Chebyshev
+//     distance fields of the last 8 threshold windows (LRU)
 //   * one packed float4 gradient volume per operator (Kernel 1, lazily)
 //   * scratch for the host-facing render path.
 // The reference API is stateless per call (raycast.py:431-438); keeping the

@@ -9,9 +9,17 @@
 // reference's operation order (see vc_device.cuh).
 //
 // B200 mapping
-//   * block = 128 threads = 4 warps, each warp an 8x4 pixel tile, the block
-//     a 16x8 screen tile: neighbouring rays share voxel cache lines in L1.
-//   * empty-space skipping over an 8^3 macrocell grid replaces the
+//   * two persistent kernels per frame (a wavefront split): firsthit_kernel
+//     generates rays, marches to the first in-window lattice sample, refines
+//     it and queues the hit; shade_kernel pulls hits, shades and composites
+//     front to back with early ray termination.  Each sizes its grid to the
+//     resident CTAs of 148 SMs and tunes its own register budget.
+//   * work is handed out per lane through warp-aggregated atomic tickets in
+//     8x4 screen tiles (a refilled warp traces a compact tile: L1 reuse), and
+//     finished lanes are refilled at once (dynamic ray scheduling), so warps
+//     stay full although rays march very different lengths; warp votes
+//     decide when a warp leaves its march loop.
+//   * empty-space skipping over a 4^3 macrocell grid replaces the
 //     reference's octree (octree.py, _kernels.py:227-364).  It only jumps
 //     over lattice samples t_enter + k*coarse that provably lie in cells
 //     whose 8 corners are all outside the threshold window, so the
@@ -19,9 +27,10 @@
 //     march (the invariant of pkg/tests/test_render.py:125-139).
 //   * the shading gradient comes either from the reference taps or from
 //     the packed float4 volume of Kernel 1 (interior only; the 1-voxel
-//     boundary band always uses the taps).
-//   * warp-vote retirement: per-warp sample / shade counters are reduced
-//     with __reduce_add_sync and committed with one atomic per warp.
+//     boundary band always uses the taps); the scalar field either from the
+//     float64 software cascade or from tex3D (VC_SAMPLER_TEXTURE).
+//   * per-warp sample / shade counters are reduced with __reduce_add_sync
+//     and committed with one atomic per warp.
 #include <cfloat>
 #include <cmath>
 #include <type_traits>
