@@ -241,13 +241,93 @@ __global__ void png_scan_kernel(const uint32_t* __restrict__ row_bytes, int heig
     }
 }
 
+// ---- CRC-32 (PNG / zlib polynomial, reflected 0xEDB88320) on the device --
+// Rows are byte strings (sync flush), so the IDAT CRC is the CRC of their
+// concatenation: each row's CRC is computed in the gather kernel (256
+// threads: per-thread chunks combined in a tree) and the row CRCs are
+// combined in a tree over the rows with crc(A||B) = crc(A) * x^(8|B|) ^
+// crc(B) in GF(2)[x]/P (the zlib crc32_combine identity).
+__device__ __forceinline__ uint32_t gf2_multmodp(uint32_t a, uint32_t b) {
+    uint32_t m = 1u << 31, p = 0;
+    for (;;) {
+        if (a & m) {
+            p ^= b;
+            if ((a & (m - 1)) == 0) break;
+        }
+        m >>= 1;
+        b = (b & 1) ? (b >> 1) ^ 0xEDB88320u : b >> 1;
+    }
+    return p;
+}
+// x^(8 n) mod P, from x2n[k] = x^(2^k) mod P
+__device__ __forceinline__ uint32_t gf2_x8n(const uint32_t* x2n, unsigned long long n) {
+    uint32_t p = 1u << 31;  // x^0
+    int k = 3;
+    while (n) {
+        if (n & 1) p = gf2_multmodp(x2n[k & 31], p);
+        n >>= 1;
+        k++;
+    }
+    return p;
+}
+__device__ __forceinline__ uint32_t crc_combine(const uint32_t* x2n, uint32_t c1, uint32_t c2,
+                                                unsigned long long len2) {
+    return gf2_multmodp(gf2_x8n(x2n, len2), c1) ^ c2;
+}
+
 __global__ void png_gather_kernel(const uint32_t* __restrict__ rowbuf, size_t row_words,
                                   const uint32_t* __restrict__ row_bytes,
-                                  const unsigned long long* __restrict__ offsets, uint8_t* __restrict__ out) {
+                                  const unsigned long long* __restrict__ offsets, uint8_t* __restrict__ out,
+                                  const uint32_t* __restrict__ crc_table, const uint32_t* __restrict__ x2n_g,
+                                  uint32_t* __restrict__ row_crc) {
+    __shared__ uint32_t tab[256], x2n[32];
+    __shared__ uint32_t part[256];
+    __shared__ uint32_t plen[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = crc_table[i];
+    if (threadIdx.x < 32) x2n[threadIdx.x] = x2n_g[threadIdx.x];
+    __syncthreads();
     const int y = blockIdx.x;
     const uint8_t* src = reinterpret_cast<const uint8_t*>(rowbuf + (size_t)y * row_words);
     uint8_t* dst = out + offsets[y];
-    for (uint32_t i = threadIdx.x; i < row_bytes[y]; i += blockDim.x) dst[i] = src[i];
+    const uint32_t nb = row_bytes[y];
+    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) dst[i] = src[i];
+    // per-thread contiguous chunk CRC (standard pre/post conditioning)
+    const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
+    const uint32_t a = min(nb, threadIdx.x * per), b = min(nb, a + per);
+    uint32_t c = 0xFFFFFFFFu;
+    for (uint32_t i = a; i < b; i++) c = tab[(c ^ src[i]) & 0xFF] ^ (c >> 8);
+    part[threadIdx.x] = c ^ 0xFFFFFFFFu;
+    plen[threadIdx.x] = b - a;
+    __syncthreads();
+    for (int step = 1; step < (int)blockDim.x; step <<= 1) {  // ordered tree combine
+        const int t = threadIdx.x;
+        if ((t % (2 * step)) == 0 && t + step < (int)blockDim.x) {
+            part[t] = plen[t + step] ? crc_combine(x2n, part[t], part[t + step], plen[t + step]) : part[t];
+            plen[t] += plen[t + step];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) row_crc[y] = part[0];
+}
+
+// ordered tree combine of the row CRCs (one block, in place over levels)
+__global__ void png_crc_rows_kernel(uint32_t* __restrict__ crc, const uint32_t* __restrict__ row_bytes,
+                                    int height, const uint32_t* __restrict__ x2n_g,
+                                    unsigned long long* __restrict__ lens, uint32_t* __restrict__ result) {
+    __shared__ uint32_t x2n[32];
+    if (threadIdx.x < 32) x2n[threadIdx.x] = x2n_g[threadIdx.x];
+    for (int i = threadIdx.x; i < height; i += blockDim.x) lens[i] = row_bytes[i];
+    __syncthreads();
+    for (int step = 1; step < height; step <<= 1) {
+        for (int t = threadIdx.x * 2 * step; t < height; t += blockDim.x * 2 * step) {
+            if (t + step < height) {
+                crc[t] = lens[t + step] ? crc_combine(x2n, crc[t], crc[t + step], lens[t + step]) : crc[t];
+                lens[t] += lens[t + step];
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *result = crc[0];
 }
 
 }  // namespace vc
@@ -256,6 +336,21 @@ namespace {
 
 uint32_t crc_tab[8][256];
 bool crc_ready = false;
+uint32_t x2n_tab[32];  // x^(2^k) mod P (zlib crc32_combine tables)
+
+uint32_t multmodp_host(uint32_t a, uint32_t b) {
+    uint32_t m = 1u << 31, p = 0;
+    for (;;) {
+        if (a & m) {
+            p ^= b;
+            if ((a & (m - 1)) == 0) break;
+        }
+        m >>= 1;
+        b = (b & 1) ? (b >> 1) ^ 0xEDB88320u : b >> 1;
+    }
+    return p;
+}
+
 
 void crc_init() {  // slice-by-8 tables of the PNG CRC-32 (polynomial 0xEDB88320)
     for (uint32_t n = 0; n < 256; n++) {
@@ -265,6 +360,9 @@ void crc_init() {  // slice-by-8 tables of the PNG CRC-32 (polynomial 0xEDB88320
     }
     for (uint32_t n = 0; n < 256; n++)
         for (int t = 1; t < 8; t++) crc_tab[t][n] = (crc_tab[t - 1][n] >> 8) ^ crc_tab[0][crc_tab[t - 1][n] & 0xFF];
+    uint32_t p = 1u << 30;  // x^1
+    x2n_tab[0] = p;
+    for (int k = 1; k < 32; k++) x2n_tab[k] = p = multmodp_host(p, p);
     crc_ready = true;
 }
 
@@ -286,19 +384,19 @@ uint32_t crc32(const uint8_t* p, size_t n, uint32_t c = 0) {
     return c ^ 0xFFFFFFFFu;
 }
 
-void be32(std::vector<uint8_t>& v, uint32_t x) {
-    v.push_back(x >> 24);
-    v.push_back(x >> 16);
-    v.push_back(x >> 8);
-    v.push_back(x);
+uint32_t crc32_combine_host(uint32_t c1, uint32_t c2, unsigned long long len2) {
+    uint32_t p = 1u << 31;
+    int k = 3;
+    for (unsigned long long n = len2; n; n >>= 1, k++)
+        if (n & 1) p = multmodp_host(x2n_tab[k & 31], p);
+    return multmodp_host(p, c1) ^ c2;
 }
 
-void chunk(std::vector<uint8_t>& out, const char* type, const uint8_t* data, size_t n) {
-    be32(out, (uint32_t)n);
-    const size_t start = out.size();
-    out.insert(out.end(), type, type + 4);
-    out.insert(out.end(), data, data + n);
-    be32(out, crc32(out.data() + start, n + 4));
+void put_be32(uint8_t* o, uint32_t x) {
+    o[0] = x >> 24;
+    o[1] = x >> 16;
+    o[2] = x >> 8;
+    o[3] = x;
 }
 
 }  // namespace
@@ -310,23 +408,29 @@ extern "C" VC_API int vc_encode_png(const uint8_t* d_rgba, int width, int height
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t n = 1 + 3 * (size_t)width;
     const size_t row_words = (n * 9 / 8 + 64) / 4 + 4;
-    uint32_t *rowbuf = nullptr, *row_bytes = nullptr;
-    unsigned long long *adler = nullptr, *offsets = nullptr;
+    uint32_t *rowbuf = nullptr, *row_bytes = nullptr, *row_crc = nullptr, *tables = nullptr;
+    unsigned long long *adler = nullptr, *offsets = nullptr, *lens = nullptr;
     uint8_t* packed = nullptr;
     int rc = VC_OK;
     auto ok = [&](cudaError_t e) {
         if (e != cudaSuccess && rc == VC_OK) rc = VC_ERR_CUDA;
         return e == cudaSuccess;
     };
+    if (!crc_ready) crc_init();
     ok(cudaMallocAsync((void**)&rowbuf, row_words * 4 * height, s));
     ok(cudaMallocAsync((void**)&row_bytes, 4 * (size_t)height, s));
+    ok(cudaMallocAsync((void**)&row_crc, 4 * (size_t)height + 4, s));
+    ok(cudaMallocAsync((void**)&tables, 4 * (256 + 32), s));
     ok(cudaMallocAsync((void**)&adler, 16 * (size_t)height, s));
     ok(cudaMallocAsync((void**)&offsets, 8 * (size_t)(height + 1), s));
+    ok(cudaMallocAsync((void**)&lens, 8 * (size_t)height, s));
     ok(cudaMallocAsync((void**)&packed, row_words * 4 * height, s));
-    std::vector<uint8_t> zdata;
     std::vector<unsigned long long> hadler(2 * (size_t)height);
     unsigned long long total = 0;
+    uint32_t rows_crc = 0;
     if (rc == VC_OK) {
+        ok(cudaMemcpyAsync(tables, crc_tab[0], 4 * 256, cudaMemcpyHostToDevice, s));
+        ok(cudaMemcpyAsync(tables + 256, x2n_tab, 4 * 32, cudaMemcpyHostToDevice, s));
         const size_t smem = PNG_ROWS_PER_BLOCK * ((n + 15) & ~(size_t)15);
         if (smem > 48 * 1024)
             ok(cudaFuncSetAttribute(png_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -334,49 +438,66 @@ extern "C" VC_API int vc_encode_png(const uint8_t* d_rgba, int width, int height
                           s>>>(d_rgba, width, height, rowbuf, row_words, row_bytes, adler);
         ok(cudaGetLastError());
         png_scan_kernel<<<1, 1024, 0, s>>>(row_bytes, height, offsets);
-        png_gather_kernel<<<height, 256, 0, s>>>(rowbuf, row_words, row_bytes, offsets, packed);
+        png_gather_kernel<<<height, 256, 0, s>>>(rowbuf, row_words, row_bytes, offsets, packed, tables,
+                                                 tables + 256, row_crc);
+        png_crc_rows_kernel<<<1, 1024, 0, s>>>(row_crc, row_bytes, height, tables + 256, lens,
+                                               row_crc + height);
         ok(cudaGetLastError());
         ok(cudaMemcpyAsync(&total, offsets + height, 8, cudaMemcpyDeviceToHost, s));
+        ok(cudaMemcpyAsync(&rows_crc, row_crc + height, 4, cudaMemcpyDeviceToHost, s));
         ok(cudaMemcpyAsync(hadler.data(), adler, 16 * (size_t)height, cudaMemcpyDeviceToHost, s));
         ok(cudaStreamSynchronize(s));
     }
-    if (rc == VC_OK) {
-        zdata.resize(2 + total + 4);
-        zdata[0] = 0x78;
-        zdata[1] = 0x01;
-        ok(cudaMemcpyAsync(zdata.data() + 2, packed, total, cudaMemcpyDeviceToHost, s));
-        ok(cudaStreamSynchronize(s));
-        // Adler-32 of all filtered rows
+    // file layout: signature, IHDR, IDAT {78 01, rows, Adler-32}, IEND
+    const size_t idat_len = 2 + (size_t)total + 4;
+    const size_t file_len = 8 + 25 + 8 + idat_len + 4 + 12;
+    *out_len = file_len;
+    if (rc == VC_OK && h_out != nullptr && h_cap >= file_len) {
+        uint8_t* o = h_out;
+        const uint8_t sig[8] = {0x89, 'P', 'N', 'G', '\r', '\n', 0x1A, '\n'};
+        memcpy(o, sig, 8);
+        const uint32_t W = (uint32_t)width, H = (uint32_t)height;
+        const uint8_t ihdr[4 + 4 + 13] = {0, 0, 0, 13, 'I', 'H', 'D', 'R',
+                                          (uint8_t)(W >> 24), (uint8_t)(W >> 16), (uint8_t)(W >> 8), (uint8_t)W,
+                                          (uint8_t)(H >> 24), (uint8_t)(H >> 16), (uint8_t)(H >> 8), (uint8_t)H,
+                                          8, 2, 0, 0, 0};
+        memcpy(o + 8, ihdr, sizeof(ihdr));
+        put_be32(o + 8 + 21, crc32(ihdr + 4, 17));
+        uint8_t* id = o + 33;  // IDAT chunk
+        put_be32(id, (uint32_t)idat_len);
+        memcpy(id + 4, "IDAT", 4);
+        id[8] = 0x78;
+        id[9] = 0x01;
+        // the compressed rows go straight from HBM into the caller's buffer
+        ok(cudaMemcpyAsync(id + 10, packed, total, cudaMemcpyDeviceToHost, s));
+        // Adler-32 of all filtered rows (per-row sums from the device)
         unsigned long long A = 1, B = 0;
         for (int y = 0; y < height; y++) {
             B = (B + (n % 65521) * A + hadler[2 * y + 1] % 65521) % 65521;
             A = (A + hadler[2 * y] % 65521) % 65521;
         }
-        const uint32_t ad = (uint32_t)((B << 16) | A);
-        zdata[2 + total + 0] = ad >> 24;
-        zdata[2 + total + 1] = ad >> 16;
-        zdata[2 + total + 2] = ad >> 8;
-        zdata[2 + total + 3] = ad;
+        uint8_t ad[4];
+        put_be32(ad, (uint32_t)((B << 16) | A));
+        // CRC over "IDAT", the zlib header, the rows (device) and the Adler
+        uint32_t c = crc32(id + 4, 6);
+        c = crc32_combine_host(c, rows_crc, total);
+        c = crc32(ad, 4, c);
+        ok(cudaStreamSynchronize(s));
+        memcpy(id + 10 + total, ad, 4);
+        put_be32(id + 10 + total + 4, c);
+        uint8_t* ie = id + 10 + total + 8;
+        const uint8_t iend[12] = {0, 0, 0, 0, 'I', 'E', 'N', 'D', 0xAE, 0x42, 0x60, 0x82};
+        memcpy(ie, iend, 12);
     }
     cudaFreeAsync(rowbuf, s);
     cudaFreeAsync(row_bytes, s);
+    cudaFreeAsync(row_crc, s);
+    cudaFreeAsync(tables, s);
     cudaFreeAsync(adler, s);
     cudaFreeAsync(offsets, s);
+    cudaFreeAsync(lens, s);
     cudaFreeAsync(packed, s);
     if (rc != VC_OK) return rc;
-    std::vector<uint8_t> png = {0x89, 'P', 'N', 'G', '\r', '\n', 0x1A, '\n'};
-    uint8_t ihdr[13];
-    const uint32_t W = (uint32_t)width, H = (uint32_t)height;
-    const uint8_t hdr[13] = {(uint8_t)(W >> 24), (uint8_t)(W >> 16), (uint8_t)(W >> 8), (uint8_t)W,
-                             (uint8_t)(H >> 24), (uint8_t)(H >> 16), (uint8_t)(H >> 8), (uint8_t)H,
-                             8, 2, 0, 0, 0};
-    memcpy(ihdr, hdr, 13);
-    chunk(png, "IHDR", ihdr, 13);
-    chunk(png, "IDAT", zdata.data(), zdata.size());
-    chunk(png, "IEND", nullptr, 0);
-    *out_len = png.size();
-    if (h_out == nullptr) return VC_OK;  // size query
-    if (h_cap < png.size()) return VC_ERR_INVALID;
-    memcpy(h_out, png.data(), png.size());
+    if (h_out != nullptr && h_cap < file_len) return VC_ERR_INVALID;
     return VC_OK;
 }

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes
 import struct
+import threading
 
 import numpy as np
 
@@ -18,14 +19,27 @@ from .raycast import FrameBuffer, RenderSettings, Scene, prepare_device, render_
 from .volume import Volume
 
 
+_out_bufs: dict = {}
+_out_lock = threading.Lock()
+
+
 def _encode_device(ptr: int, width: int, height: int, stream: int = 0) -> bytes:
+    """Encode on the device into a reused pinned host buffer (the compressed
+    rows are DMA'd straight into it), return one bytes copy of the file."""
+    import torch
+
     L = _native.load()
     cap = 64 + height * ((1 + 3 * width) * 9 // 8 + 32)
-    buf = ctypes.create_string_buffer(cap)
     n = ctypes.c_size_t(0)
-    _native.check(L.vc_encode_png(ctypes.c_void_p(ptr), int(width), int(height), ctypes.c_void_p(stream),
-                                  buf, cap, ctypes.byref(n)))
-    return buf.raw[:n.value]
+    with _out_lock:
+        buf = _out_bufs.get(cap)
+        if buf is None:
+            if len(_out_bufs) > 4:
+                _out_bufs.clear()
+            buf = _out_bufs[cap] = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+        _native.check(L.vc_encode_png(ctypes.c_void_p(ptr), int(width), int(height), ctypes.c_void_p(stream),
+                                      ctypes.c_void_p(buf.data_ptr()), cap, ctypes.byref(n)))
+        return buf.numpy()[: n.value].tobytes()
 
 
 def png_bytes(pixels, device: int = 0) -> bytes:

@@ -403,10 +403,14 @@ def test_device_png_round_trip(wh):
     while pos < len(png):
         n = int.from_bytes(png[pos:pos + 4], "big")
         typ = png[pos + 4:pos + 8]
+        # every chunk's CRC-32 (the IDAT one is combined from per-row CRCs
+        # computed on the device)
+        assert int.from_bytes(png[pos + 8 + n:pos + 12 + n], "big") == zlib.crc32(png[pos + 4:pos + 8 + n])
         if typ == b"IDAT":
             raw = zlib.decompress(png[pos + 8:pos + 8 + n])
             assert len(raw) == H * (1 + 3 * W)
         pos += 12 + n
+    assert pos == len(png)
 
 
 def test_render_frame_png_matches_render_frame():
