@@ -11,14 +11,15 @@
 //   * deflate: one fixed-Huffman block per scanline, one warp per scanline;
 //     the 32 lanes tokenize 32 slices of the filtered row in parallel
 //     (literals + distance-1 / distance-3 matches: zero runs over
-//     background, repeating RGB along flat shading), a
-//     warp scan of the bit counts places every lane's codes, and lanes OR
-//     their bits into the row's output words;
+//     background, repeating RGB along flat shading), a warp scan of the
+//     bit counts places every lane's codes, and each lane writes its words
+//     from a register bit buffer (atomics only on the two words it may
+//     share with its neighbours);
 //   * rows end with a sync flush (empty stored block) so the per-row
 //     streams are byte aligned and simply concatenated (device scan +
 //     gather); the last row carries BFINAL;
 //   * Adler-32: per-row sums on the device, combined on the host; CRC-32 of
-//     the (small) IDAT payload on the host.
+//     the rows on the device (see png_gather_kernel).
 // The result is a standard PNG (zlib stream, 8-bit RGB) any decoder reads.
 #include <cstring>
 #include <vector>
@@ -71,16 +72,43 @@ __device__ __forceinline__ void length_sym(int L, int& sym, int& ebits, int& eva
     (void)base;
 }
 
+// LSB-first bit writer of one lane's slice of a row.  Bits gather in a
+// 64-bit register and leave as whole 32-bit words: plain stores for the
+// words only this lane writes, atomicOr for the first and last word, which
+// it may share with the neighbouring lanes' slices (the row's words start
+// zeroed).  A null `words` only counts.
 struct BitSink {
     uint32_t* words;
-    uint64_t pos;
-    __device__ __forceinline__ void put(uint32_t bits, int n) {  // LSB-first
+    uint64_t pos;             // absolute bit position of the next bit
+    uint64_t acc = 0;         // pending bits, aligned to word (pos0 >> 5) of `first`
+    int nacc = 0;             // bits in acc, counted from the word boundary
+    uint64_t wnext = 0;       // word index acc[0..31] belongs to
+    bool first = true;        // the next word flushed is this lane's first (shared) word
+    __device__ __forceinline__ void begin() {
+        wnext = pos >> 5;
+        nacc = (int)(pos & 31);
+        acc = 0;
+        first = true;
+    }
+    __device__ __forceinline__ void put(uint32_t bits, int n) {
         if (n == 0) return;
-        const uint64_t w = pos >> 5;
-        const int off = (int)(pos & 31);
-        atomicOr(words + w, bits << off);
-        if (off + n > 32) atomicOr(words + w + 1, bits >> (32 - off));
+        acc |= (uint64_t)bits << nacc;
+        nacc += n;
         pos += n;
+        if (nacc >= 32) {
+            if (first) {
+                atomicOr(words + wnext, (uint32_t)acc);
+                first = false;
+            } else {
+                words[wnext] = (uint32_t)acc;
+            }
+            acc >>= 32;
+            nacc -= 32;
+            wnext++;
+        }
+    }
+    __device__ __forceinline__ void finish() {  // last partial word: shared with the next slice
+        if (nacc > 0) atomicOr(words + wnext, (uint32_t)acc);
     }
 };
 
@@ -131,22 +159,33 @@ __device__ uint64_t encode_slice(const uint8_t* d, int a, int b, bool emit, BitS
     return bits;
 }
 
-constexpr int PNG_ROWS_PER_BLOCK = 4;
+// One CTA per scanline, PNG_SEGS warps: the CTA filters the row once into
+// shared memory, then warp w deflates segment w of it as its own
+// fixed-Huffman block ending in a sync flush (byte aligned), so the
+// segments concatenate like rows do.  Matches may reach back into the
+// previous segment (the decoder's window holds it).  Measured at 1080p:
+// 1 / 2 / 4 / 8 segments -> 0.64 / 0.50 / 0.44 / 0.42 ms, 2.06 / 2.10 /
+// 2.20 / 2.37 MB (runs are cut at every lane slice): 2 it is.
+#ifndef VC_PNG_SEGS
+#define VC_PNG_SEGS 2
+#endif
+constexpr int PNG_SEGS = VC_PNG_SEGS;
 
-__global__ void __launch_bounds__(32 * PNG_ROWS_PER_BLOCK) png_rows_kernel(
-    const uint8_t* __restrict__ rgba, int width, int height, uint32_t* __restrict__ rowbuf, size_t row_words,
-    uint32_t* __restrict__ row_bytes, unsigned long long* __restrict__ adler) {
-    extern __shared__ uint8_t sm[];
+__host__ __device__ inline size_t png_seg_words(size_t n) { return ((n + PNG_SEGS - 1) / PNG_SEGS * 9 / 8 + 64) / 4 + 4; }
+
+__global__ void __launch_bounds__(32 * PNG_SEGS) png_rows_kernel(
+    const uint8_t* __restrict__ rgba, int width, int height, uint32_t* __restrict__ segbuf, size_t seg_words,
+    uint32_t* __restrict__ seg_bytes, unsigned long long* __restrict__ adler) {
+    extern __shared__ uint8_t d[];
+    __shared__ unsigned long long red[2][PNG_SEGS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int y = blockIdx.x * PNG_ROWS_PER_BLOCK + warp;
+    const int y = blockIdx.x;
     const int n = 1 + 3 * width;
-    uint8_t* d = sm + (size_t)warp * ((n + 15) & ~15);
-    if (y >= height) return;
     // Up-filtered RGB scanline
     const uint8_t* cur = rgba + (size_t)y * width * 4;
     const uint8_t* prev = y > 0 ? rgba + (size_t)(y - 1) * width * 4 : nullptr;
-    if (lane == 0) d[0] = 2;
-    for (int x = lane; x < width; x += 32) {
+    if (threadIdx.x == 0) d[0] = 2;
+    for (int x = threadIdx.x; x < width; x += blockDim.x) {
         const uchar4 c = *reinterpret_cast<const uchar4*>(cur + 4 * x);
         uchar4 p = make_uchar4(0, 0, 0, 0);
         if (prev) p = *reinterpret_cast<const uchar4*>(prev + 4 * x);
@@ -154,10 +193,10 @@ __global__ void __launch_bounds__(32 * PNG_ROWS_PER_BLOCK) png_rows_kernel(
         d[2 + 3 * x] = (uint8_t)(c.y - p.y);
         d[3 + 3 * x] = (uint8_t)(c.z - p.z);
     }
-    __syncwarp();
-    // Adler-32 pieces: sum b_i and sum (n - i) b_i
+    __syncthreads();
+    // Adler-32 pieces of the row: sum b_i and sum (n - i) b_i
     unsigned long long sa = 0, sb = 0;
-    for (int i = lane; i < n; i += 32) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
         sa += d[i];
         sb += (unsigned long long)(n - i) * d[i];
     }
@@ -166,50 +205,64 @@ __global__ void __launch_bounds__(32 * PNG_ROWS_PER_BLOCK) png_rows_kernel(
         sb += __shfl_xor_sync(0xffffffffu, sb, o);
     }
     if (lane == 0) {
-        adler[2 * y] = sa;
-        adler[2 * y + 1] = sb;
+        red[0][warp] = sa;
+        red[1][warp] = sb;
     }
-    // tokenize 32 slices; bits per lane, warp exclusive scan
-    const int a = (int)((long long)n * lane / 32), b = (int)((long long)n * (lane + 1) / 32);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long A = 0, B = 0;
+        for (int w = 0; w < PNG_SEGS; w++) {
+            A += red[0][w];
+            B += red[1][w];
+        }
+        adler[2 * y] = A;
+        adler[2 * y + 1] = B;
+    }
+    // this warp's segment [s0, s1), tokenized in 32 lane slices
+    const int s0 = (int)((long long)n * warp / PNG_SEGS), s1 = (int)((long long)n * (warp + 1) / PNG_SEGS);
+    const int len = s1 - s0;
+    const int a = s0 + (int)((long long)len * lane / 32), b = s0 + (int)((long long)len * (lane + 1) / 32);
     BitSink dummy{nullptr, 0};
-    const uint64_t mybits = encode_slice(d, a, b, false, dummy);
+    const uint64_t mybits = encode_slice(d, a, b, false, dummy);  // counting pass
     uint64_t incl = mybits;
     for (int o = 1; o < 32; o <<= 1) {
         const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += v;
     }
     const uint64_t total = __shfl_sync(0xffffffffu, incl, 31);
-    uint32_t* words = rowbuf + (size_t)y * row_words;
-    for (size_t w = lane; w < row_words; w += 32) words[w] = 0;
+    const size_t seg = (size_t)y * PNG_SEGS + warp;
+    uint32_t* words = segbuf + seg * seg_words;
+    for (size_t w = lane; w < seg_words; w += 32) words[w] = 0;
     __syncwarp();
-    const bool last = (y == height - 1);
-    BitSink s{words, 3 + (incl - mybits)};
-    if (lane == 0) {
-        BitSink h{words, 0};
-        h.put(last ? 1u : 0u, 1);  // BFINAL
-        h.put(1u, 2);              // BTYPE = 01, fixed Huffman
+    const bool last = (y == height - 1) && warp == PNG_SEGS - 1;
+    BitSink bs{words, 3 + (incl - mybits)};
+    bs.begin();
+    if (lane == 0) {  // block header: BFINAL, BTYPE = 01 (fixed Huffman)
+        atomicOr(words, (last ? 1u : 0u) | (1u << 1));
     }
-    encode_slice(d, a, b, true, s);
+    encode_slice(d, a, b, true, bs);
+    bs.finish();
     __syncwarp();
     if (lane == 0) {
         BitSink t{words, 3 + total};
+        t.begin();
         uint32_t code;
-        int len;
-        lit_code(256, code, len);  // end of block
-        t.put(code, len);
+        int clen;
+        lit_code(256, code, clen);  // end of block
+        t.put(code, clen);
+        t.finish();
         uint64_t nbits = t.pos;
         if (!last) {  // sync flush: empty stored block, byte aligned, 00 00 FF FF
-            t.put(0u, 3);
-            nbits = (t.pos + 7) & ~7ull;
+            nbits = (t.pos + 3 + 7) & ~7ull;  // 3 zero header bits (words start zeroed), then pad
             uint8_t* bytes = reinterpret_cast<uint8_t*>(words);
             const size_t nb = nbits >> 3;
             bytes[nb + 0] = 0x00;
             bytes[nb + 1] = 0x00;
             bytes[nb + 2] = 0xFF;
             bytes[nb + 3] = 0xFF;
-            row_bytes[y] = (uint32_t)(nb + 4);
+            seg_bytes[seg] = (uint32_t)(nb + 4);
         } else {
-            row_bytes[y] = (uint32_t)((nbits + 7) >> 3);
+            seg_bytes[seg] = (uint32_t)((nbits + 7) >> 3);
         }
     }
 }
@@ -259,75 +312,69 @@ __device__ __forceinline__ uint32_t gf2_multmodp(uint32_t a, uint32_t b) {
     }
     return p;
 }
-// x^(8 n) mod P, from x2n[k] = x^(2^k) mod P
-__device__ __forceinline__ uint32_t gf2_x8n(const uint32_t* x2n, unsigned long long n) {
-    uint32_t p = 1u << 31;  // x^0
-    int k = 3;
-    while (n) {
-        if (n & 1) p = gf2_multmodp(x2n[k & 31], p);
-        n >>= 1;
-        k++;
-    }
-    return p;
-}
-__device__ __forceinline__ uint32_t crc_combine(const uint32_t* x2n, uint32_t c1, uint32_t c2,
-                                                unsigned long long len2) {
-    return gf2_multmodp(gf2_x8n(x2n, len2), c1) ^ c2;
-}
-
 __global__ void png_gather_kernel(const uint32_t* __restrict__ rowbuf, size_t row_words,
                                   const uint32_t* __restrict__ row_bytes,
-                                  const unsigned long long* __restrict__ offsets, uint8_t* __restrict__ out,
-                                  const uint32_t* __restrict__ crc_table, const uint32_t* __restrict__ x2n_g,
-                                  uint32_t* __restrict__ row_crc) {
-    __shared__ uint32_t tab[256], x2n[32];
-    __shared__ uint32_t part[256];
-    __shared__ uint32_t plen[256];
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = crc_table[i];
-    if (threadIdx.x < 32) x2n[threadIdx.x] = x2n_g[threadIdx.x];
-    __syncthreads();
+                                  const unsigned long long* __restrict__ offsets, uint8_t* __restrict__ out) {
     const int y = blockIdx.x;
     const uint8_t* src = reinterpret_cast<const uint8_t*>(rowbuf + (size_t)y * row_words);
     uint8_t* dst = out + offsets[y];
-    const uint32_t nb = row_bytes[y];
-    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) dst[i] = src[i];
-    // per-thread contiguous chunk CRC (standard pre/post conditioning)
-    const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
-    const uint32_t a = min(nb, threadIdx.x * per), b = min(nb, a + per);
-    uint32_t c = 0xFFFFFFFFu;
-    for (uint32_t i = a; i < b; i++) c = tab[(c ^ src[i]) & 0xFF] ^ (c >> 8);
-    part[threadIdx.x] = c ^ 0xFFFFFFFFu;
-    plen[threadIdx.x] = b - a;
-    __syncthreads();
-    for (int step = 1; step < (int)blockDim.x; step <<= 1) {  // ordered tree combine
-        const int t = threadIdx.x;
-        if ((t % (2 * step)) == 0 && t + step < (int)blockDim.x) {
-            part[t] = plen[t + step] ? crc_combine(x2n, part[t], part[t + step], plen[t + step]) : part[t];
-            plen[t] += plen[t + step];
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) row_crc[y] = part[0];
+    for (uint32_t i = threadIdx.x; i < row_bytes[y]; i += blockDim.x) dst[i] = src[i];
 }
 
-// ordered tree combine of the row CRCs (one block, in place over levels)
-__global__ void png_crc_rows_kernel(uint32_t* __restrict__ crc, const uint32_t* __restrict__ row_bytes,
-                                    int height, const uint32_t* __restrict__ x2n_g,
-                                    unsigned long long* __restrict__ lens, uint32_t* __restrict__ result) {
-    __shared__ uint32_t x2n[32];
+// CRC-32 of the gathered stream, fully parallel.  The raw CRC (register
+// starting at 0, no final xor) is linear, raw(A||B) = raw(A) * x^(8|B|) ^
+// raw(B) in GF(2)[x]/P, and leading zero bytes do not change it.  So the
+// stream is virtually front-padded with zeros to a power-of-two number of
+// CRC_BLOCK-byte blocks: every pair in both combine trees (8-byte thread
+// chunks inside a block, then blocks) has a full right half, and each level
+// multiplies by one fixed power x^(2^k) -- one multmodp per pair.  The
+// host turns the raw value into the PNG CRC: raw ^ 0xFFFFFFFF * x^(8 n) ^
+// 0xFFFFFFFF.
+constexpr int CRC_BLOCK = 2048;  // 256 threads x 8 bytes
+
+__global__ void __launch_bounds__(256) png_crc_blocks_kernel(const uint8_t* __restrict__ data,
+                                                             const unsigned long long* __restrict__ total_p,
+                                                             const uint32_t* __restrict__ crc_table,
+                                                             const uint32_t* __restrict__ x2n_g,
+                                                             uint32_t* __restrict__ block_crc) {
+    __shared__ uint32_t tab[256], x2n[32], part[256];
+    const long long total = (long long)*total_p;
+    long long nb = (total + CRC_BLOCK - 1) / CRC_BLOCK, nbp = 1;
+    while (nbp < nb) nbp <<= 1;
+    if ((long long)blockIdx.x >= nbp) return;
+    const long long pad = nbp * CRC_BLOCK - total;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = crc_table[i];
     if (threadIdx.x < 32) x2n[threadIdx.x] = x2n_g[threadIdx.x];
-    for (int i = threadIdx.x; i < height; i += blockDim.x) lens[i] = row_bytes[i];
     __syncthreads();
-    for (int step = 1; step < height; step <<= 1) {
-        for (int t = threadIdx.x * 2 * step; t < height; t += blockDim.x * 2 * step) {
-            if (t + step < height) {
-                crc[t] = lens[t + step] ? crc_combine(x2n, crc[t], crc[t + step], lens[t + step]) : crc[t];
-                lens[t] += lens[t + step];
-            }
-        }
+    // bytes [a, a + 8) of the padded stream = [a - pad, a - pad + 8) of the data
+    const long long a = (long long)blockIdx.x * CRC_BLOCK + 8ll * threadIdx.x - pad;
+    uint32_t c = 0;  // raw register; the leading pad zeros leave it at 0
+    for (long long i = max(a, 0ll); i < a + 8; i++) c = tab[(c ^ data[i]) & 0xFF] ^ (c >> 8);
+    part[threadIdx.x] = c;
+    __syncthreads();
+    for (int L = 0; L < 8; L++) {  // right halves of 8 * 2^L bytes
+        const int t = threadIdx.x, st = 1 << L;
+        if ((t & (2 * st - 1)) == 0) part[t] = gf2_multmodp(x2n[6 + L], part[t]) ^ part[t + st];
         __syncthreads();
     }
-    if (threadIdx.x == 0) *result = crc[0];
+    if (threadIdx.x == 0) block_crc[blockIdx.x] = part[0];
+}
+
+__global__ void png_crc_tree_kernel(uint32_t* __restrict__ crc, const unsigned long long* __restrict__ total_p,
+                                    const uint32_t* __restrict__ x2n_g, uint32_t* __restrict__ result) {
+    __shared__ uint32_t x2n[32];
+    if (threadIdx.x < 32) x2n[threadIdx.x] = x2n_g[threadIdx.x];
+    __syncthreads();
+    const long long total = (long long)*total_p;
+    long long nb = (total + CRC_BLOCK - 1) / CRC_BLOCK, nbp = 1;
+    while (nbp < nb) nbp <<= 1;
+    for (int L = 0; (1ll << L) < nbp; L++) {  // right halves of CRC_BLOCK * 2^L bytes
+        const long long st = 1ll << L;
+        for (long long t = threadIdx.x * 2 * st; t < nbp; t += (long long)blockDim.x * 2 * st)
+            crc[t] = gf2_multmodp(x2n[(14 + L) & 31], crc[t]) ^ crc[t + st];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *result = total > 0 ? crc[0] : 0u;
 }
 
 }  // namespace vc
@@ -384,12 +431,17 @@ uint32_t crc32(const uint8_t* p, size_t n, uint32_t c = 0) {
     return c ^ 0xFFFFFFFFu;
 }
 
-uint32_t crc32_combine_host(uint32_t c1, uint32_t c2, unsigned long long len2) {
+// c * x^(8 len) mod P
+uint32_t shift_host(uint32_t c, unsigned long long len) {
     uint32_t p = 1u << 31;
     int k = 3;
-    for (unsigned long long n = len2; n; n >>= 1, k++)
+    for (unsigned long long n = len; n; n >>= 1, k++)
         if (n & 1) p = multmodp_host(x2n_tab[k & 31], p);
-    return multmodp_host(p, c1) ^ c2;
+    return multmodp_host(p, c);
+}
+
+uint32_t crc32_combine_host(uint32_t c1, uint32_t c2, unsigned long long len2) {
+    return shift_host(c1, len2) ^ c2;
 }
 
 void put_be32(uint8_t* o, uint32_t x) {
@@ -407,9 +459,10 @@ extern "C" VC_API int vc_encode_png(const uint8_t* d_rgba, int width, int height
     if (!d_rgba || !out_len || width <= 0 || height <= 0) return VC_ERR_INVALID;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t n = 1 + 3 * (size_t)width;
-    const size_t row_words = (n * 9 / 8 + 64) / 4 + 4;
+    const size_t row_words = png_seg_words(n);  // per segment
+    const int nseg = height * PNG_SEGS;
     uint32_t *rowbuf = nullptr, *row_bytes = nullptr, *row_crc = nullptr, *tables = nullptr;
-    unsigned long long *adler = nullptr, *offsets = nullptr, *lens = nullptr;
+    unsigned long long *adler = nullptr, *offsets = nullptr;
     uint8_t* packed = nullptr;
     int rc = VC_OK;
     auto ok = [&](cudaError_t e) {
@@ -417,34 +470,36 @@ extern "C" VC_API int vc_encode_png(const uint8_t* d_rgba, int width, int height
         return e == cudaSuccess;
     };
     if (!crc_ready) crc_init();
-    ok(cudaMallocAsync((void**)&rowbuf, row_words * 4 * height, s));
-    ok(cudaMallocAsync((void**)&row_bytes, 4 * (size_t)height, s));
-    ok(cudaMallocAsync((void**)&row_crc, 4 * (size_t)height + 4, s));
+    ok(cudaMallocAsync((void**)&rowbuf, row_words * 4 * nseg, s));
+    ok(cudaMallocAsync((void**)&row_bytes, 4 * (size_t)nseg, s));
+    // block CRCs of the gathered stream (upper bound on its size) + the result
+    size_t max_blocks = 1;  // power of two >= the stream's block count (upper bound)
+    while (max_blocks * CRC_BLOCK < row_words * 4 * (size_t)nseg) max_blocks <<= 1;
+    ok(cudaMallocAsync((void**)&row_crc, 4 * max_blocks + 4, s));
     ok(cudaMallocAsync((void**)&tables, 4 * (256 + 32), s));
     ok(cudaMallocAsync((void**)&adler, 16 * (size_t)height, s));
-    ok(cudaMallocAsync((void**)&offsets, 8 * (size_t)(height + 1), s));
-    ok(cudaMallocAsync((void**)&lens, 8 * (size_t)height, s));
-    ok(cudaMallocAsync((void**)&packed, row_words * 4 * height, s));
+    ok(cudaMallocAsync((void**)&offsets, 8 * (size_t)(nseg + 1), s));
+    ok(cudaMallocAsync((void**)&packed, row_words * 4 * nseg, s));
     std::vector<unsigned long long> hadler(2 * (size_t)height);
     unsigned long long total = 0;
     uint32_t rows_crc = 0;
     if (rc == VC_OK) {
         ok(cudaMemcpyAsync(tables, crc_tab[0], 4 * 256, cudaMemcpyHostToDevice, s));
         ok(cudaMemcpyAsync(tables + 256, x2n_tab, 4 * 32, cudaMemcpyHostToDevice, s));
-        const size_t smem = PNG_ROWS_PER_BLOCK * ((n + 15) & ~(size_t)15);
+        const size_t smem = (n + 15) & ~(size_t)15;
         if (smem > 48 * 1024)
             ok(cudaFuncSetAttribute(png_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        png_rows_kernel<<<(height + PNG_ROWS_PER_BLOCK - 1) / PNG_ROWS_PER_BLOCK, 32 * PNG_ROWS_PER_BLOCK, smem,
-                          s>>>(d_rgba, width, height, rowbuf, row_words, row_bytes, adler);
+        png_rows_kernel<<<height, 32 * PNG_SEGS, smem, s>>>(d_rgba, width, height, rowbuf, row_words, row_bytes,
+                                                           adler);
         ok(cudaGetLastError());
-        png_scan_kernel<<<1, 1024, 0, s>>>(row_bytes, height, offsets);
-        png_gather_kernel<<<height, 256, 0, s>>>(rowbuf, row_words, row_bytes, offsets, packed, tables,
-                                                 tables + 256, row_crc);
-        png_crc_rows_kernel<<<1, 1024, 0, s>>>(row_crc, row_bytes, height, tables + 256, lens,
-                                               row_crc + height);
+        png_scan_kernel<<<1, 1024, 0, s>>>(row_bytes, nseg, offsets);
+        png_gather_kernel<<<nseg, 256, 0, s>>>(rowbuf, row_words, row_bytes, offsets, packed);
+        png_crc_blocks_kernel<<<(unsigned)max_blocks, 256, 0, s>>>(packed, offsets + nseg, tables, tables + 256,
+                                                                   row_crc);
+        png_crc_tree_kernel<<<1, 1024, 0, s>>>(row_crc, offsets + nseg, tables + 256, row_crc + max_blocks);
         ok(cudaGetLastError());
-        ok(cudaMemcpyAsync(&total, offsets + height, 8, cudaMemcpyDeviceToHost, s));
-        ok(cudaMemcpyAsync(&rows_crc, row_crc + height, 4, cudaMemcpyDeviceToHost, s));
+        ok(cudaMemcpyAsync(&total, offsets + nseg, 8, cudaMemcpyDeviceToHost, s));
+        ok(cudaMemcpyAsync(&rows_crc, row_crc + max_blocks, 4, cudaMemcpyDeviceToHost, s));
         ok(cudaMemcpyAsync(hadler.data(), adler, 16 * (size_t)height, cudaMemcpyDeviceToHost, s));
         ok(cudaStreamSynchronize(s));
     }
@@ -479,8 +534,10 @@ extern "C" VC_API int vc_encode_png(const uint8_t* d_rgba, int width, int height
         uint8_t ad[4];
         put_be32(ad, (uint32_t)((B << 16) | A));
         // CRC over "IDAT", the zlib header, the rows (device) and the Adler
+        // the device's raw CRC of the rows -> their PNG CRC, then chain
+        const uint32_t rows_std = rows_crc ^ shift_host(0xFFFFFFFFu, total) ^ 0xFFFFFFFFu;
         uint32_t c = crc32(id + 4, 6);
-        c = crc32_combine_host(c, rows_crc, total);
+        c = crc32_combine_host(c, rows_std, total);
         c = crc32(ad, 4, c);
         ok(cudaStreamSynchronize(s));
         memcpy(id + 10 + total, ad, 4);
@@ -495,7 +552,6 @@ extern "C" VC_API int vc_encode_png(const uint8_t* d_rgba, int width, int height
     cudaFreeAsync(tables, s);
     cudaFreeAsync(adler, s);
     cudaFreeAsync(offsets, s);
-    cudaFreeAsync(lens, s);
     cudaFreeAsync(packed, s);
     if (rc != VC_OK) return rc;
     if (h_out != nullptr && h_cap < file_len) return VC_ERR_INVALID;

@@ -29,7 +29,7 @@ def _encode_device(ptr: int, width: int, height: int, stream: int = 0) -> bytes:
     import torch
 
     L = _native.load()
-    cap = 64 + height * ((1 + 3 * width) * 9 // 8 + 32)
+    cap = 64 + height * ((1 + 3 * width) * 9 // 8 + 64)  # + per-row block framing (segments)
     n = ctypes.c_size_t(0)
     with _out_lock:
         buf = _out_bufs.get(cap)
