@@ -171,7 +171,9 @@ __device__ uint64_t encode_slice(const uint8_t* d, int a, int b, bool emit, BitS
 #endif
 constexpr int PNG_SEGS = VC_PNG_SEGS;
 
-__host__ __device__ inline size_t png_seg_words(size_t n) { return ((n + PNG_SEGS - 1) / PNG_SEGS * 9 / 8 + 64) / 4 + 4; }
+// segments per row: 2 from 1024 pixels on (small rows keep one block)
+__host__ __device__ inline int png_segs(int width) { return width >= 1024 ? PNG_SEGS : 1; }
+__host__ __device__ inline size_t png_seg_words(size_t n, int segs) { return ((n + segs - 1) / segs * 9 / 8 + 64) / 4 + 4; }
 
 __global__ void __launch_bounds__(32 * PNG_SEGS) png_rows_kernel(
     const uint8_t* __restrict__ rgba, int width, int height, uint32_t* __restrict__ segbuf, size_t seg_words,
@@ -179,6 +181,7 @@ __global__ void __launch_bounds__(32 * PNG_SEGS) png_rows_kernel(
     extern __shared__ uint8_t d[];
     __shared__ unsigned long long red[2][PNG_SEGS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int segs = (int)(blockDim.x >> 5);
     const int y = blockIdx.x;
     const int n = 1 + 3 * width;
     // Up-filtered RGB scanline
@@ -211,7 +214,7 @@ __global__ void __launch_bounds__(32 * PNG_SEGS) png_rows_kernel(
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long A = 0, B = 0;
-        for (int w = 0; w < PNG_SEGS; w++) {
+        for (int w = 0; w < segs; w++) {
             A += red[0][w];
             B += red[1][w];
         }
@@ -219,7 +222,7 @@ __global__ void __launch_bounds__(32 * PNG_SEGS) png_rows_kernel(
         adler[2 * y + 1] = B;
     }
     // this warp's segment [s0, s1), tokenized in 32 lane slices
-    const int s0 = (int)((long long)n * warp / PNG_SEGS), s1 = (int)((long long)n * (warp + 1) / PNG_SEGS);
+    const int s0 = (int)((long long)n * warp / segs), s1 = (int)((long long)n * (warp + 1) / segs);
     const int len = s1 - s0;
     const int a = s0 + (int)((long long)len * lane / 32), b = s0 + (int)((long long)len * (lane + 1) / 32);
     BitSink dummy{nullptr, 0};
@@ -230,11 +233,11 @@ __global__ void __launch_bounds__(32 * PNG_SEGS) png_rows_kernel(
         if (lane >= o) incl += v;
     }
     const uint64_t total = __shfl_sync(0xffffffffu, incl, 31);
-    const size_t seg = (size_t)y * PNG_SEGS + warp;
+    const size_t seg = (size_t)y * segs + warp;
     uint32_t* words = segbuf + seg * seg_words;
     for (size_t w = lane; w < seg_words; w += 32) words[w] = 0;
     __syncwarp();
-    const bool last = (y == height - 1) && warp == PNG_SEGS - 1;
+    const bool last = (y == height - 1) && warp == segs - 1;
     BitSink bs{words, 3 + (incl - mybits)};
     bs.begin();
     if (lane == 0) {  // block header: BFINAL, BTYPE = 01 (fixed Huffman)
@@ -459,8 +462,9 @@ extern "C" VC_API int vc_encode_png(const uint8_t* d_rgba, int width, int height
     if (!d_rgba || !out_len || width <= 0 || height <= 0) return VC_ERR_INVALID;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t n = 1 + 3 * (size_t)width;
-    const size_t row_words = png_seg_words(n);  // per segment
-    const int nseg = height * PNG_SEGS;
+    const int segs = png_segs(width);
+    const size_t row_words = png_seg_words(n, segs);  // per segment
+    const int nseg = height * segs;
     uint32_t *rowbuf = nullptr, *row_bytes = nullptr, *row_crc = nullptr, *tables = nullptr;
     unsigned long long *adler = nullptr, *offsets = nullptr;
     uint8_t* packed = nullptr;
@@ -489,8 +493,8 @@ extern "C" VC_API int vc_encode_png(const uint8_t* d_rgba, int width, int height
         const size_t smem = (n + 15) & ~(size_t)15;
         if (smem > 48 * 1024)
             ok(cudaFuncSetAttribute(png_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        png_rows_kernel<<<height, 32 * PNG_SEGS, smem, s>>>(d_rgba, width, height, rowbuf, row_words, row_bytes,
-                                                           adler);
+        png_rows_kernel<<<height, 32 * segs, smem, s>>>(d_rgba, width, height, rowbuf, row_words, row_bytes,
+                                                        adler);
         ok(cudaGetLastError());
         png_scan_kernel<<<1, 1024, 0, s>>>(row_bytes, nseg, offsets);
         png_gather_kernel<<<nseg, 256, 0, s>>>(rowbuf, row_words, row_bytes, offsets, packed);
