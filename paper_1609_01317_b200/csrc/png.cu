@@ -2,54 +2,40 @@
 //
 // The reference ships frames to its viewer as PNG (image_io.png_bytes,
 // image_io.py:52-55, via Pillow/zlib on one CPU core; service.py:180-202),
-// which at 1080p costs tens of milliseconds -- far more than rendering the
-// frame here.  This encoder keeps the frame in HBM and copies only the
+// which at 1080p costs hundreds of milliseconds -- far more than rendering
+// the frame here.  This encoder keeps the frame in HBM and copies only the
 // compressed bytes to the host:
 //
-//   * filter: PNG "Up" on every scanline (prior row of row 0 = zeros),
-//     RGB from the RGBA frame (alpha dropped like image_io._as_rgb);
-//   * deflate: one fixed-Huffman block per scanline, one warp per scanline;
-//     the 32 lanes tokenize 32 slices of the filtered row in parallel
-//     (literals + distance-1 / distance-3 matches: zero runs over
-//     background, repeating RGB along flat shading), a warp scan of the
-//     bit counts places every lane's codes, and each lane writes its words
-//     from a register bit buffer (atomics only on the two words it may
-//     share with its neighbours);
-//   * rows end with a sync flush (empty stored block) so the per-row
-//     streams are byte aligned and simply concatenated (device scan +
-//     gather); the last row carries BFINAL;
+//   * filter: PNG "Up" on every scanline (prior row of row 0 = zeros), RGB
+//     from the RGBA frame (alpha dropped like image_io._as_rgb);
+//   * tokens: one CTA per scanline, each of its TOK_LANES threads tokenizes
+//     a slice of the filtered row (literals + distance-1 / distance-3
+//     matches: zero runs over background, repeating RGB along flat shading)
+//     into a token buffer and a shared symbol histogram;
+//   * code: the frame is ONE dynamic-Huffman deflate block.  The host turns
+//     the histogram into length-limited canonical codes (zlib-style) and
+//     the block header; every thread then knows its bit count, a scan gives
+//     its bit offset, and all threads write their codes in parallel at those
+//     offsets (whole words from a register bit buffer, atomics only on the
+//     two words a slice may share with its neighbours);
 //   * Adler-32: per-row sums on the device, combined on the host; CRC-32 of
-//     the rows on the device (see png_gather_kernel).
-// The result is a standard PNG (zlib stream, 8-bit RGB) any decoder reads.
+//     the stream on the device (block tree, see png_crc_blocks_kernel).
+// The result is a standard PNG (zlib stream, 8-bit RGB) any decoder reads;
+// one shared table makes it about as small as zlib level 6.
+#include <algorithm>
 #include <cstring>
+#include <iterator>
 #include <vector>
 
 #include "vc_internal.h"
 
 namespace vc {
 
-// fixed Huffman code of a literal / length symbol (RFC 1951 3.2.6), bit-reversed
-// so it can be emitted LSB-first
-__device__ __forceinline__ void lit_code(int sym, uint32_t& code, int& len) {
-    uint32_t c;
-    if (sym < 144) {
-        c = 0x30 + sym;
-        len = 8;
-    } else if (sym < 256) {
-        c = 0x190 + (sym - 144);
-        len = 9;
-    } else if (sym < 280) {
-        c = sym - 256;
-        len = 7;
-    } else {
-        c = 0xC0 + (sym - 280);
-        len = 8;
-    }
-    code = __brev(c) >> (32 - len);
-}
+constexpr int TOK_LANES = 64;  // tokenizing threads per scanline
+constexpr int NLIT = 286, NDIST = 30;
 
-// length 3..258 -> (symbol, extra bits, extra value)
-__device__ __forceinline__ void length_sym(int L, int& sym, int& ebits, int& eval) {
+// length 3..258 -> (symbol, extra bits, extra value), RFC 1951 3.2.5
+__host__ __device__ inline void length_sym(int L, int& sym, int& ebits, int& eval) {
     if (L == 258) {
         sym = 285;
         ebits = 0;
@@ -63,27 +49,29 @@ __device__ __forceinline__ void length_sym(int L, int& sym, int& ebits, int& eva
         eval = 0;
         return;
     }
-    // groups of 4 lengths per extra-bit count
-    int eb = 31 - __clz(v) - 2;  // v in [2^(eb+2), 2^(eb+3))
-    int base = (4 << eb);        // first v of the group... (v >> eb) in [4, 8)
+    int eb = 0;  // v in [2^(eb+2), 2^(eb+3))
+    while ((v >> (eb + 3)) != 0) eb++;
     sym = 257 + 4 * eb + 4 + ((v >> eb) - 4);
     ebits = eb;
     eval = v - ((v >> eb) << eb);
-    (void)base;
 }
 
-// LSB-first bit writer of one lane's slice of a row.  Bits gather in a
-// 64-bit register and leave as whole 32-bit words: plain stores for the
-// words only this lane writes, atomicOr for the first and last word, which
-// it may share with the neighbouring lanes' slices (the row's words start
-// zeroed).  A null `words` only counts.
+// token: symbol (9 bits) | extra-bit count (3) | extra value (5) | distance (2: 0 none, 1 -> d=1, 2 -> d=3)
+__device__ __forceinline__ uint32_t make_token(int sym, int eb, int ev, int dist) {
+    return (uint32_t)sym | ((uint32_t)eb << 9) | ((uint32_t)ev << 12) | ((uint32_t)dist << 17);
+}
+
+// LSB-first bit writer of one thread's slice of the stream.  Bits gather in a
+// 64-bit register and leave as whole 32-bit words: plain stores for words
+// only this thread writes, atomicOr for its first and last word, which it
+// may share with its neighbours (the buffer starts zeroed).
 struct BitSink {
     uint32_t* words;
-    uint64_t pos;             // absolute bit position of the next bit
-    uint64_t acc = 0;         // pending bits, aligned to word (pos0 >> 5) of `first`
-    int nacc = 0;             // bits in acc, counted from the word boundary
-    uint64_t wnext = 0;       // word index acc[0..31] belongs to
-    bool first = true;        // the next word flushed is this lane's first (shared) word
+    uint64_t pos;
+    uint64_t acc = 0;
+    int nacc = 0;
+    uint64_t wnext = 0;
+    bool first = true;
     __device__ __forceinline__ void begin() {
         wnext = pos >> 5;
         nacc = (int)(pos & 31);
@@ -107,19 +95,56 @@ struct BitSink {
             wnext++;
         }
     }
-    __device__ __forceinline__ void finish() {  // last partial word: shared with the next slice
+    __device__ __forceinline__ void finish() {
         if (nacc > 0) atomicOr(words + wnext, (uint32_t)acc);
     }
 };
 
-// token pass over [a, b) of row data d; emit == false only counts bits.
-// Greedy LZ77 with two candidate distances: 1 (byte runs -- Up-filtered
-// rows of unchanged pixels are zero runs) and 3 (the previous RGB pixel --
-// flat or repeating colour along the row).  Matches may reach back before
-// a (the decoder already has those bytes) but not before the row start.
-__device__ uint64_t encode_slice(const uint8_t* d, int a, int b, bool emit, BitSink& s) {
-    uint64_t bits = 0;
-    int i = a;
+__host__ __device__ inline int tok_slice_max(int n) { return (n + TOK_LANES - 1) / TOK_LANES + 1; }
+
+// Filter + tokenize one scanline per CTA.  Greedy LZ77 with two candidate
+// distances, 1 (byte runs -- Up-filtered rows of unchanged pixels are zero
+// runs) and 3 (the previous RGB pixel); a match may reach back before the
+// slice (the decoder has those bytes) but not before the row start.
+__global__ void __launch_bounds__(TOK_LANES) png_tokenize_kernel(
+    const uint8_t* __restrict__ rgba, int width, int height, uint32_t* __restrict__ tokens,
+    uint32_t* __restrict__ ntok, unsigned int* __restrict__ hist, unsigned long long* __restrict__ adler) {
+    extern __shared__ uint8_t d[];
+    __shared__ unsigned int h[NLIT + NDIST];
+    __shared__ unsigned long long red[2][TOK_LANES / 32];
+    const int y = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int n = 1 + 3 * width;
+    for (int i = t; i < NLIT + NDIST; i += blockDim.x) h[i] = 0;
+    const uint8_t* cur = rgba + (size_t)y * width * 4;
+    const uint8_t* prev = y > 0 ? rgba + (size_t)(y - 1) * width * 4 : nullptr;
+    if (t == 0) d[0] = 2;  // filter type Up
+    for (int x = t; x < width; x += blockDim.x) {
+        const uchar4 c = *reinterpret_cast<const uchar4*>(cur + 4 * x);
+        uchar4 p = make_uchar4(0, 0, 0, 0);
+        if (prev) p = *reinterpret_cast<const uchar4*>(prev + 4 * x);
+        d[1 + 3 * x] = (uint8_t)(c.x - p.x);
+        d[2 + 3 * x] = (uint8_t)(c.y - p.y);
+        d[3 + 3 * x] = (uint8_t)(c.z - p.z);
+    }
+    __syncthreads();
+    // Adler-32 pieces of the row: sum b_i and sum (n - i) b_i
+    unsigned long long sa = 0, sb = 0;
+    for (int i = t; i < n; i += blockDim.x) {
+        sa += d[i];
+        sb += (unsigned long long)(n - i) * d[i];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        sb += __shfl_xor_sync(0xffffffffu, sb, o);
+    }
+    if (lane == 0) {
+        red[0][warp] = sa;
+        red[1][warp] = sb;
+    }
+    // this thread's slice
+    const int a = (int)((long long)n * t / TOK_LANES), b = (int)((long long)n * (t + 1) / TOK_LANES);
+    uint32_t* out = tokens + ((size_t)y * TOK_LANES + t) * tok_slice_max(n);
+    int k = 0, i = a;
     while (i < b) {
         int best = 0, dist = 0;
         if (i >= 1) {
@@ -136,148 +161,121 @@ __device__ uint64_t encode_slice(const uint8_t* d, int a, int b, bool emit, BitS
                 dist = 3;
             }
         }
-        uint32_t code;
-        int len;
         if (best >= 3) {
             int sym, eb, ev;
             length_sym(best, sym, eb, ev);
-            lit_code(sym, code, len);
-            bits += len + eb + 5;
-            if (emit) {
-                s.put(code, len);
-                s.put((uint32_t)ev, eb);
-                s.put(dist == 1 ? 0u : 0x08u, 5);  // distance codes 0 (d=1) and 2 (d=3), bit-reversed
-            }
+            out[k++] = make_token(sym, eb, ev, dist == 1 ? 1 : 2);
+            atomicAdd(&h[sym], 1u);
+            atomicAdd(&h[NLIT + (dist == 1 ? 0 : 2)], 1u);  // distance codes 0 (d=1), 2 (d=3)
             i += best;
         } else {
-            lit_code(d[i], code, len);
-            bits += len;
-            if (emit) s.put(code, len);
+            out[k++] = make_token(d[i], 0, 0, 0);
+            atomicAdd(&h[d[i]], 1u);
             i += 1;
         }
     }
-    return bits;
-}
-
-// One CTA per scanline, PNG_SEGS warps: the CTA filters the row once into
-// shared memory, then warp w deflates segment w of it as its own
-// fixed-Huffman block ending in a sync flush (byte aligned), so the
-// segments concatenate like rows do.  Matches may reach back into the
-// previous segment (the decoder's window holds it).  Measured at 1080p:
-// 1 / 2 / 4 / 8 segments -> 0.64 / 0.50 / 0.44 / 0.42 ms, 2.06 / 2.10 /
-// 2.20 / 2.37 MB (runs are cut at every lane slice): 2 it is.
-#ifndef VC_PNG_SEGS
-#define VC_PNG_SEGS 2
-#endif
-constexpr int PNG_SEGS = VC_PNG_SEGS;
-
-// segments per row: 2 from 1024 pixels on (small rows keep one block)
-__host__ __device__ inline int png_segs(int width) { return width >= 1024 ? PNG_SEGS : 1; }
-__host__ __device__ inline size_t png_seg_words(size_t n, int segs) { return ((n + segs - 1) / segs * 9 / 8 + 64) / 4 + 4; }
-
-__global__ void __launch_bounds__(32 * PNG_SEGS) png_rows_kernel(
-    const uint8_t* __restrict__ rgba, int width, int height, uint32_t* __restrict__ segbuf, size_t seg_words,
-    uint32_t* __restrict__ seg_bytes, unsigned long long* __restrict__ adler) {
-    extern __shared__ uint8_t d[];
-    __shared__ unsigned long long red[2][PNG_SEGS];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int segs = (int)(blockDim.x >> 5);
-    const int y = blockIdx.x;
-    const int n = 1 + 3 * width;
-    // Up-filtered RGB scanline
-    const uint8_t* cur = rgba + (size_t)y * width * 4;
-    const uint8_t* prev = y > 0 ? rgba + (size_t)(y - 1) * width * 4 : nullptr;
-    if (threadIdx.x == 0) d[0] = 2;
-    for (int x = threadIdx.x; x < width; x += blockDim.x) {
-        const uchar4 c = *reinterpret_cast<const uchar4*>(cur + 4 * x);
-        uchar4 p = make_uchar4(0, 0, 0, 0);
-        if (prev) p = *reinterpret_cast<const uchar4*>(prev + 4 * x);
-        d[1 + 3 * x] = (uint8_t)(c.x - p.x);
-        d[2 + 3 * x] = (uint8_t)(c.y - p.y);
-        d[3 + 3 * x] = (uint8_t)(c.z - p.z);
-    }
+    ntok[(size_t)y * TOK_LANES + t] = (uint32_t)k;
     __syncthreads();
-    // Adler-32 pieces of the row: sum b_i and sum (n - i) b_i
-    unsigned long long sa = 0, sb = 0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        sa += d[i];
-        sb += (unsigned long long)(n - i) * d[i];
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        sa += __shfl_xor_sync(0xffffffffu, sa, o);
-        sb += __shfl_xor_sync(0xffffffffu, sb, o);
-    }
-    if (lane == 0) {
-        red[0][warp] = sa;
-        red[1][warp] = sb;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    if (t == 0) {
         unsigned long long A = 0, B = 0;
-        for (int w = 0; w < segs; w++) {
+        for (int w = 0; w < TOK_LANES / 32; w++) {
             A += red[0][w];
             B += red[1][w];
         }
         adler[2 * y] = A;
         adler[2 * y + 1] = B;
     }
-    // this warp's segment [s0, s1), tokenized in 32 lane slices
-    const int s0 = (int)((long long)n * warp / segs), s1 = (int)((long long)n * (warp + 1) / segs);
-    const int len = s1 - s0;
-    const int a = s0 + (int)((long long)len * lane / 32), b = s0 + (int)((long long)len * (lane + 1) / 32);
-    BitSink dummy{nullptr, 0};
-    const uint64_t mybits = encode_slice(d, a, b, false, dummy);  // counting pass
-    uint64_t incl = mybits;
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-    }
-    const uint64_t total = __shfl_sync(0xffffffffu, incl, 31);
-    const size_t seg = (size_t)y * segs + warp;
-    uint32_t* words = segbuf + seg * seg_words;
-    for (size_t w = lane; w < seg_words; w += 32) words[w] = 0;
-    __syncwarp();
-    const bool last = (y == height - 1) && warp == segs - 1;
-    BitSink bs{words, 3 + (incl - mybits)};
-    bs.begin();
-    if (lane == 0) {  // block header: BFINAL, BTYPE = 01 (fixed Huffman)
-        atomicOr(words, (last ? 1u : 0u) | (1u << 1));
-    }
-    encode_slice(d, a, b, true, bs);
-    bs.finish();
-    __syncwarp();
-    if (lane == 0) {
-        BitSink t{words, 3 + total};
-        t.begin();
-        uint32_t code;
-        int clen;
-        lit_code(256, code, clen);  // end of block
-        t.put(code, clen);
-        t.finish();
-        uint64_t nbits = t.pos;
-        if (!last) {  // sync flush: empty stored block, byte aligned, 00 00 FF FF
-            nbits = (t.pos + 3 + 7) & ~7ull;  // 3 zero header bits (words start zeroed), then pad
-            uint8_t* bytes = reinterpret_cast<uint8_t*>(words);
-            const size_t nb = nbits >> 3;
-            bytes[nb + 0] = 0x00;
-            bytes[nb + 1] = 0x00;
-            bytes[nb + 2] = 0xFF;
-            bytes[nb + 3] = 0xFF;
-            seg_bytes[seg] = (uint32_t)(nb + 4);
-        } else {
-            seg_bytes[seg] = (uint32_t)((nbits + 7) >> 3);
-        }
-    }
+    for (int s = t; s < NLIT + NDIST; s += blockDim.x)
+        if (h[s]) atomicAdd(&hist[s], h[s]);
 }
 
-// exclusive scan of row byte counts (one block)
-__global__ void png_scan_kernel(const uint32_t* __restrict__ row_bytes, int height,
+// Huffman code tables from the host: code (bit-reversed for LSB-first
+// output) in the low 16 bits, length in the high 16
+struct CodeTables {
+    uint32_t lit[NLIT];
+    uint32_t dist[NDIST];
+};
+
+__device__ __forceinline__ uint32_t token_bits(const CodeTables& c, uint32_t tk) {
+    const int sym = tk & 511, eb = (tk >> 9) & 7, dist = (tk >> 17) & 3;
+    uint32_t bits = (c.lit[sym] >> 16) + eb;
+    if (dist) bits += c.dist[dist == 1 ? 0 : 2] >> 16;
+    return bits;
+}
+
+// bit count of every slice, exclusive prefix within its row and the row total
+__global__ void __launch_bounds__(TOK_LANES) png_bits_kernel(const uint32_t* __restrict__ tokens,
+                                                             const uint32_t* __restrict__ ntok, int n,
+                                                             const CodeTables* __restrict__ codes,
+                                                             uint32_t* __restrict__ slice_prefix,
+                                                             uint32_t* __restrict__ row_bits) {
+    __shared__ CodeTables c;
+    __shared__ uint32_t warp_sum[TOK_LANES / 32];
+    for (int i = threadIdx.x; i < NLIT + NDIST; i += blockDim.x) (&c.lit[0])[i] = (&codes->lit[0])[i];
+    __syncthreads();
+    const size_t s = (size_t)blockIdx.x * TOK_LANES + threadIdx.x;
+    const uint32_t* tk = tokens + s * tok_slice_max(n);
+    uint32_t bits = 0;
+    for (uint32_t k = 0; k < ntok[s]; k++) bits += token_bits(c, tk[k]);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = bits;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) warp_sum[warp] = incl;
+    __syncthreads();
+    uint32_t before = 0;
+    for (int w = 0; w < warp; w++) before += warp_sum[w];
+    slice_prefix[s] = before + incl - bits;
+    if (threadIdx.x == blockDim.x - 1) row_bits[blockIdx.x] = before + incl;
+}
+
+__global__ void __launch_bounds__(TOK_LANES) png_emit_kernel(const uint32_t* __restrict__ tokens,
+                                                             const uint32_t* __restrict__ ntok, int n,
+                                                             const CodeTables* __restrict__ codes,
+                                                             const unsigned long long* __restrict__ row_offsets,
+                                                             const uint32_t* __restrict__ slice_prefix,
+                                                             uint64_t header_bits, uint32_t* __restrict__ words) {
+    __shared__ CodeTables c;
+    for (int i = threadIdx.x; i < NLIT + NDIST; i += blockDim.x) (&c.lit[0])[i] = (&codes->lit[0])[i];
+    __syncthreads();
+    const size_t s = (size_t)blockIdx.x * TOK_LANES + threadIdx.x;
+    const uint32_t* tk = tokens + s * tok_slice_max(n);
+    BitSink bs{words, header_bits + row_offsets[blockIdx.x] + slice_prefix[s]};
+    bs.begin();
+    for (uint32_t k = 0; k < ntok[s]; k++) {
+        const uint32_t t = tk[k];
+        const int sym = t & 511, eb = (t >> 9) & 7, ev = (t >> 12) & 31, dist = (t >> 17) & 3;
+        bs.put(c.lit[sym] & 0xFFFF, (int)(c.lit[sym] >> 16));
+        bs.put((uint32_t)ev, eb);
+        if (dist) {
+            const uint32_t dc = c.dist[dist == 1 ? 0 : 2];
+            bs.put(dc & 0xFFFF, (int)(dc >> 16));
+        }
+    }
+    bs.finish();
+}
+
+// end of block after the last slice; the stream's byte length
+__global__ void png_eob_kernel(const unsigned long long* __restrict__ offsets, int nslices, uint64_t header_bits,
+                               const CodeTables* __restrict__ codes, uint32_t* __restrict__ words,
+                               unsigned long long* __restrict__ total_bytes) {
+    BitSink bs{words, header_bits + offsets[nslices]};
+    bs.begin();
+    bs.put(codes->lit[256] & 0xFFFF, (int)(codes->lit[256] >> 16));
+    bs.finish();
+    *total_bytes = (bs.pos + 7) >> 3;
+}
+
+// exclusive scan of the row bit counts (one block); offsets[count] = total
+__global__ void png_scan_kernel(const uint32_t* __restrict__ vals, int count,
                                 unsigned long long* __restrict__ offsets) {
     __shared__ unsigned long long part[1024];
     const int t = threadIdx.x;
-    const int per = (height + blockDim.x - 1) / blockDim.x;
+    const int per = (count + blockDim.x - 1) / blockDim.x;
     unsigned long long s = 0;
-    for (int i = t * per; i < min(height, (t + 1) * per); i++) s += row_bytes[i];
+    for (int i = t * per; i < min(count, (t + 1) * per); i++) s += vals[i];
     part[t] = s;
     __syncthreads();
     if (t == 0) {
@@ -287,22 +285,18 @@ __global__ void png_scan_kernel(const uint32_t* __restrict__ row_bytes, int heig
             part[i] = run;
             run += v;
         }
-        offsets[height] = run;
+        offsets[count] = run;
     }
     __syncthreads();
     unsigned long long run = part[t];
-    for (int i = t * per; i < min(height, (t + 1) * per); i++) {
+    for (int i = t * per; i < min(count, (t + 1) * per); i++) {
         offsets[i] = run;
-        run += row_bytes[i];
+        run += vals[i];
     }
 }
 
 // ---- CRC-32 (PNG / zlib polynomial, reflected 0xEDB88320) on the device --
-// Rows are byte strings (sync flush), so the IDAT CRC is the CRC of their
-// concatenation: each row's CRC is computed in the gather kernel (256
-// threads: per-thread chunks combined in a tree) and the row CRCs are
-// combined in a tree over the rows with crc(A||B) = crc(A) * x^(8|B|) ^
-// crc(B) in GF(2)[x]/P (the zlib crc32_combine identity).
+// a * b in GF(2)[x] / P, reflected bit order (zlib's multmodp)
 __device__ __forceinline__ uint32_t gf2_multmodp(uint32_t a, uint32_t b) {
     uint32_t m = 1u << 31, p = 0;
     for (;;) {
@@ -315,23 +309,14 @@ __device__ __forceinline__ uint32_t gf2_multmodp(uint32_t a, uint32_t b) {
     }
     return p;
 }
-__global__ void png_gather_kernel(const uint32_t* __restrict__ rowbuf, size_t row_words,
-                                  const uint32_t* __restrict__ row_bytes,
-                                  const unsigned long long* __restrict__ offsets, uint8_t* __restrict__ out) {
-    const int y = blockIdx.x;
-    const uint8_t* src = reinterpret_cast<const uint8_t*>(rowbuf + (size_t)y * row_words);
-    uint8_t* dst = out + offsets[y];
-    for (uint32_t i = threadIdx.x; i < row_bytes[y]; i += blockDim.x) dst[i] = src[i];
-}
 
-// CRC-32 of the gathered stream, fully parallel.  The raw CRC (register
-// starting at 0, no final xor) is linear, raw(A||B) = raw(A) * x^(8|B|) ^
-// raw(B) in GF(2)[x]/P, and leading zero bytes do not change it.  So the
-// stream is virtually front-padded with zeros to a power-of-two number of
-// CRC_BLOCK-byte blocks: every pair in both combine trees (8-byte thread
+// The raw CRC (register starting at 0, no final xor) is linear, raw(A||B) =
+// raw(A) * x^(8|B|) ^ raw(B), and leading zero bytes do not change it.  So
+// the stream is virtually front-padded with zeros to a power-of-two number
+// of CRC_BLOCK-byte blocks: every pair in both combine trees (8-byte thread
 // chunks inside a block, then blocks) has a full right half, and each level
-// multiplies by one fixed power x^(2^k) -- one multmodp per pair.  The
-// host turns the raw value into the PNG CRC: raw ^ 0xFFFFFFFF * x^(8 n) ^
+// multiplies by one fixed power x^(2^k) -- one multmodp per pair.  The host
+// turns the raw value into the PNG CRC: raw ^ 0xFFFFFFFF * x^(8 n) ^
 // 0xFFFFFFFF.
 constexpr int CRC_BLOCK = 2048;  // 256 threads x 8 bytes
 
@@ -384,6 +369,9 @@ __global__ void png_crc_tree_kernel(uint32_t* __restrict__ crc, const unsigned l
 
 namespace {
 
+using vc::NDIST;
+using vc::NLIT;
+
 uint32_t crc_tab[8][256];
 bool crc_ready = false;
 uint32_t x2n_tab[32];  // x^(2^k) mod P (zlib crc32_combine tables)
@@ -400,7 +388,6 @@ uint32_t multmodp_host(uint32_t a, uint32_t b) {
     }
     return p;
 }
-
 
 void crc_init() {  // slice-by-8 tables of the PNG CRC-32 (polynomial 0xEDB88320)
     for (uint32_t n = 0; n < 256; n++) {
@@ -443,15 +430,178 @@ uint32_t shift_host(uint32_t c, unsigned long long len) {
     return multmodp_host(p, c);
 }
 
-uint32_t crc32_combine_host(uint32_t c1, uint32_t c2, unsigned long long len2) {
-    return shift_host(c1, len2) ^ c2;
-}
+uint32_t crc32_combine_host(uint32_t c1, uint32_t c2, unsigned long long len2) { return shift_host(c1, len2) ^ c2; }
 
 void put_be32(uint8_t* o, uint32_t x) {
     o[0] = x >> 24;
     o[1] = x >> 16;
     o[2] = x >> 8;
     o[3] = x;
+}
+
+// ---- Huffman code construction (host) ---------------------------------
+// Huffman code lengths of the used symbols (two-queue construction over the
+// frequency-sorted leaves), limited to maxlen the way zlib does (trees.c
+// gen_bitlen: overflowing leaves go to maxlen, then the Kraft sum is
+// repaired by splitting shorter leaves); the longest codes go to the
+// rarest symbols.  A single used symbol gets length 1.
+std::vector<int> limited_lengths(const std::vector<unsigned long long>& freq, int maxlen) {
+    const int n = (int)freq.size();
+    std::vector<int> len(n, 0), used;
+    for (int i = 0; i < n; i++)
+        if (freq[i]) used.push_back(i);
+    const int m = (int)used.size();
+    if (m == 0) return len;
+    if (m == 1) {
+        len[used[0]] = 1;
+        return len;
+    }
+    std::stable_sort(used.begin(), used.end(), [&](int x, int y) { return freq[x] < freq[y]; });
+    // nodes 0..m-1 leaves (ascending weight), m..2m-2 internal; parent links
+    std::vector<unsigned long long> w(2 * m - 1);
+    std::vector<int> parent(2 * m - 1, -1);
+    for (int i = 0; i < m; i++) w[i] = freq[used[i]];
+    int li = 0, ii = m, next = m;
+    auto take = [&]() {
+        if (li < m && (ii >= next || w[li] <= w[ii])) return li++;
+        return ii++;
+    };
+    while (next < 2 * m - 1) {
+        const int x = take(), y = take();
+        w[next] = w[x] + w[y];
+        parent[x] = parent[y] = next;
+        next++;
+    }
+    std::vector<int> depth(2 * m - 1, 0);
+    for (int i = 2 * m - 3; i >= 0; i--) depth[i] = depth[parent[i]] + 1;
+    std::vector<int> bl_count(64, 0);
+    int overflow = 0;
+    for (int i = 0; i < m; i++) {
+        int d = depth[i];
+        if (d > maxlen) {
+            d = maxlen;
+            overflow++;
+        }
+        bl_count[d]++;
+    }
+    while (overflow > 0) {
+        int bits = maxlen - 1;
+        while (bl_count[bits] == 0) bits--;
+        bl_count[bits]--;
+        bl_count[bits + 1] += 2;
+        bl_count[maxlen]--;
+        overflow -= 2;
+    }
+    // lengths by count: the rarest symbols (front of `used`) get the longest
+    int k = 0;
+    for (int bits = maxlen; bits >= 1; bits--)
+        for (int c = 0; c < bl_count[bits]; c++) len[used[k++]] = bits;
+    return len;
+}
+
+// canonical codes (RFC 1951 3.2.2), bit-reversed for LSB-first output;
+// code in the low 16 bits, length in the high 16
+std::vector<uint32_t> canonical(const std::vector<int>& len) {
+    int bl_count[16] = {0}, next_code[16] = {0};
+    for (int l : len)
+        if (l) bl_count[l]++;
+    int code = 0;
+    for (int b = 1; b < 16; b++) {
+        code = (code + bl_count[b - 1]) << 1;
+        next_code[b] = code;
+    }
+    std::vector<uint32_t> out(len.size(), 0);
+    for (size_t s = 0; s < len.size(); s++) {
+        const int l = len[s];
+        if (!l) continue;
+        uint32_t c = (uint32_t)next_code[l]++, r = 0;
+        for (int i = 0; i < l; i++) r |= ((c >> i) & 1u) << (l - 1 - i);
+        out[s] = r | ((uint32_t)l << 16);
+    }
+    return out;
+}
+
+struct HostBits {
+    std::vector<uint8_t> bytes;
+    uint64_t pos = 0;
+    void put(uint32_t v, int n) {
+        for (int i = 0; i < n; i++, pos++) {
+            if ((pos >> 3) >= bytes.size()) bytes.push_back(0);
+            if ((v >> i) & 1u) bytes[pos >> 3] |= (uint8_t)(1u << (pos & 7));
+        }
+    }
+    void code(uint32_t c) { put(c & 0xFFFF, (int)(c >> 16)); }
+};
+
+// The dynamic block: tables for the symbols in `hist` and the block header
+// (BFINAL = 1, BTYPE = 2, HLIT / HDIST / HCLEN, code-length code, run-length
+// coded code lengths), RFC 1951 3.2.7.
+void build_block(const unsigned int* hist, vc::CodeTables& tabs, HostBits& hdr) {
+    std::vector<unsigned long long> lf(NLIT), df(NDIST);
+    for (int i = 0; i < NLIT; i++) lf[i] = hist[i];
+    for (int i = 0; i < NDIST; i++) df[i] = hist[NLIT + i];
+    lf[256] = 1;  // end of block
+    int nused = 0;
+    for (auto f : lf) nused += f != 0;
+    if (nused < 2) lf[0] = std::max<unsigned long long>(lf[0], 1);  // a complete literal code
+    const std::vector<int> ll = limited_lengths(lf, 15), dl = limited_lengths(df, 15);
+    const std::vector<uint32_t> lc = canonical(ll), dc = canonical(dl);
+    for (int i = 0; i < NLIT; i++) tabs.lit[i] = lc[i];
+    for (int i = 0; i < NDIST; i++) tabs.dist[i] = dc[i];
+    int hlit = NLIT, hdist = NDIST;
+    while (hlit > 257 && ll[hlit - 1] == 0) hlit--;
+    while (hdist > 1 && dl[hdist - 1] == 0) hdist--;
+    std::vector<int> seq(ll.begin(), ll.begin() + hlit);
+    seq.insert(seq.end(), dl.begin(), dl.begin() + hdist);
+    // run-length code the lengths: (symbol, extra bits, extra value)
+    struct Rl {
+        int sym, eb, ev;
+    };
+    std::vector<Rl> rl;
+    for (size_t i = 0; i < seq.size();) {
+        size_t j = i;
+        while (j < seq.size() && seq[j] == seq[i]) j++;
+        int run = (int)(j - i);
+        if (seq[i] == 0) {
+            while (run >= 11) {
+                const int r = std::min(run, 138);
+                rl.push_back({18, 7, r - 11});
+                run -= r;
+            }
+            if (run >= 3) {
+                rl.push_back({17, 3, run - 3});
+                run = 0;
+            }
+            while (run-- > 0) rl.push_back({0, 0, 0});
+        } else {
+            rl.push_back({seq[i], 0, 0});
+            run--;
+            while (run >= 3) {
+                const int r = std::min(run, 6);
+                rl.push_back({16, 2, r - 3});
+                run -= r;
+            }
+            while (run-- > 0) rl.push_back({seq[i], 0, 0});
+        }
+        i = j;
+    }
+    std::vector<unsigned long long> cf(19, 0);
+    for (const Rl& r : rl) cf[r.sym]++;
+    const std::vector<int> cl = limited_lengths(cf, 7);
+    const std::vector<uint32_t> cc = canonical(cl);
+    static const int order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+    int hclen = 19;
+    while (hclen > 4 && cl[order[hclen - 1]] == 0) hclen--;
+    hdr.put(1, 1);  // BFINAL
+    hdr.put(2, 2);  // BTYPE = 10: dynamic Huffman
+    hdr.put((uint32_t)(hlit - 257), 5);
+    hdr.put((uint32_t)(hdist - 1), 5);
+    hdr.put((uint32_t)(hclen - 4), 4);
+    for (int i = 0; i < hclen; i++) hdr.put((uint32_t)cl[order[i]], 3);
+    for (const Rl& r : rl) {
+        hdr.code(cc[r.sym]);
+        hdr.put((uint32_t)r.ev, r.eb);
+    }
 }
 
 }  // namespace
@@ -461,53 +611,78 @@ extern "C" VC_API int vc_encode_png(const uint8_t* d_rgba, int width, int height
     using namespace vc;
     if (!d_rgba || !out_len || width <= 0 || height <= 0) return VC_ERR_INVALID;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const size_t n = 1 + 3 * (size_t)width;
-    const int segs = png_segs(width);
-    const size_t row_words = png_seg_words(n, segs);  // per segment
-    const int nseg = height * segs;
-    uint32_t *rowbuf = nullptr, *row_bytes = nullptr, *row_crc = nullptr, *tables = nullptr;
-    unsigned long long *adler = nullptr, *offsets = nullptr;
-    uint8_t* packed = nullptr;
+    const int n = 1 + 3 * width;
+    const int nslices = height * TOK_LANES;
+    const size_t tok_cap = (size_t)nslices * tok_slice_max(n);
+    // bound of the block: every byte a literal of <= 15 bits, + header
+    const size_t max_bytes = (size_t)height * ((size_t)n * 15 / 8 + 8) + 4096;
+    uint32_t *tokens = nullptr, *ntok = nullptr, *slice_bits = nullptr, *row_bits = nullptr, *block_crc = nullptr,
+             *tables = nullptr;
+    unsigned int* hist = nullptr;
+    unsigned long long *adler = nullptr, *offsets = nullptr, *total_bytes = nullptr;
+    uint32_t* words = nullptr;
+    CodeTables* codes = nullptr;
     int rc = VC_OK;
     auto ok = [&](cudaError_t e) {
         if (e != cudaSuccess && rc == VC_OK) rc = VC_ERR_CUDA;
         return e == cudaSuccess;
     };
     if (!crc_ready) crc_init();
-    ok(cudaMallocAsync((void**)&rowbuf, row_words * 4 * nseg, s));
-    ok(cudaMallocAsync((void**)&row_bytes, 4 * (size_t)nseg, s));
-    // block CRCs of the gathered stream (upper bound on its size) + the result
-    size_t max_blocks = 1;  // power of two >= the stream's block count (upper bound)
-    while (max_blocks * CRC_BLOCK < row_words * 4 * (size_t)nseg) max_blocks <<= 1;
-    ok(cudaMallocAsync((void**)&row_crc, 4 * max_blocks + 4, s));
-    ok(cudaMallocAsync((void**)&tables, 4 * (256 + 32), s));
+    size_t max_blocks = 1;  // power of two >= the stream's CRC block count (upper bound)
+    while (max_blocks * CRC_BLOCK < max_bytes) max_blocks <<= 1;
+    const size_t words_bytes = (max_bytes + 8) & ~(size_t)3;
+    ok(cudaMallocAsync((void**)&tokens, tok_cap * 4, s));
+    ok(cudaMallocAsync((void**)&ntok, 4 * (size_t)nslices, s));
+    ok(cudaMallocAsync((void**)&slice_bits, 4 * (size_t)nslices, s));
+    ok(cudaMallocAsync((void**)&row_bits, 4 * (size_t)height, s));
+    ok(cudaMallocAsync((void**)&hist, 4 * (NLIT + NDIST), s));
     ok(cudaMallocAsync((void**)&adler, 16 * (size_t)height, s));
-    ok(cudaMallocAsync((void**)&offsets, 8 * (size_t)(nseg + 1), s));
-    ok(cudaMallocAsync((void**)&packed, row_words * 4 * nseg, s));
+    ok(cudaMallocAsync((void**)&offsets, 8 * ((size_t)height + 1), s));
+    ok(cudaMallocAsync((void**)&total_bytes, 8, s));
+    ok(cudaMallocAsync((void**)&words, words_bytes, s));
+    ok(cudaMallocAsync((void**)&codes, sizeof(CodeTables), s));
+    ok(cudaMallocAsync((void**)&tables, 4 * (256 + 32), s));
+    ok(cudaMallocAsync((void**)&block_crc, 4 * max_blocks + 4, s));
+    std::vector<unsigned int> hhist(NLIT + NDIST, 0);
     std::vector<unsigned long long> hadler(2 * (size_t)height);
     unsigned long long total = 0;
-    uint32_t rows_crc = 0;
-    if (rc == VC_OK) {
+    uint32_t raw_crc = 0;
+    HostBits hdr;
+    CodeTables tabs{};
+    if (rc == VC_OK) {  // pass 1: filter, tokenize, histogram
+        ok(cudaMemsetAsync(hist, 0, 4 * (NLIT + NDIST), s));
+        const size_t smem = ((size_t)n + 15) & ~(size_t)15;
+        if (smem > 40 * 1024)
+            ok(cudaFuncSetAttribute(png_tokenize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        png_tokenize_kernel<<<height, TOK_LANES, smem, s>>>(d_rgba, width, height, tokens, ntok, hist, adler);
+        ok(cudaGetLastError());
+        ok(cudaMemcpyAsync(hhist.data(), hist, 4 * (NLIT + NDIST), cudaMemcpyDeviceToHost, s));
+        ok(cudaStreamSynchronize(s));
+    }
+    if (rc == VC_OK) {  // the code and the block header; pass 2: bit counts, offsets, emission, CRC
+        build_block(hhist.data(), tabs, hdr);
+        const size_t hdr_words = (hdr.bytes.size() + 3) / 4;
+        std::vector<uint32_t> hw(hdr_words, 0);
+        memcpy(hw.data(), hdr.bytes.data(), hdr.bytes.size());
+        ok(cudaMemsetAsync(words, 0, words_bytes, s));
+        ok(cudaMemcpyAsync(words, hw.data(), hdr_words * 4, cudaMemcpyHostToDevice, s));
+        ok(cudaMemcpyAsync(codes, &tabs, sizeof(CodeTables), cudaMemcpyHostToDevice, s));
         ok(cudaMemcpyAsync(tables, crc_tab[0], 4 * 256, cudaMemcpyHostToDevice, s));
         ok(cudaMemcpyAsync(tables + 256, x2n_tab, 4 * 32, cudaMemcpyHostToDevice, s));
-        const size_t smem = (n + 15) & ~(size_t)15;
-        if (smem > 48 * 1024)
-            ok(cudaFuncSetAttribute(png_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        png_rows_kernel<<<height, 32 * segs, smem, s>>>(d_rgba, width, height, rowbuf, row_words, row_bytes,
-                                                        adler);
+        png_bits_kernel<<<height, TOK_LANES, 0, s>>>(tokens, ntok, n, codes, slice_bits, row_bits);
+        png_scan_kernel<<<1, 1024, 0, s>>>(row_bits, height, offsets);
+        png_emit_kernel<<<height, TOK_LANES, 0, s>>>(tokens, ntok, n, codes, offsets, slice_bits, hdr.pos, words);
+        png_eob_kernel<<<1, 1, 0, s>>>(offsets, height, hdr.pos, codes, words, total_bytes);
+        png_crc_blocks_kernel<<<(unsigned)max_blocks, 256, 0, s>>>(reinterpret_cast<const uint8_t*>(words),
+                                                                   total_bytes, tables, tables + 256, block_crc);
+        png_crc_tree_kernel<<<1, 1024, 0, s>>>(block_crc, total_bytes, tables + 256, block_crc + max_blocks);
         ok(cudaGetLastError());
-        png_scan_kernel<<<1, 1024, 0, s>>>(row_bytes, nseg, offsets);
-        png_gather_kernel<<<nseg, 256, 0, s>>>(rowbuf, row_words, row_bytes, offsets, packed);
-        png_crc_blocks_kernel<<<(unsigned)max_blocks, 256, 0, s>>>(packed, offsets + nseg, tables, tables + 256,
-                                                                   row_crc);
-        png_crc_tree_kernel<<<1, 1024, 0, s>>>(row_crc, offsets + nseg, tables + 256, row_crc + max_blocks);
-        ok(cudaGetLastError());
-        ok(cudaMemcpyAsync(&total, offsets + nseg, 8, cudaMemcpyDeviceToHost, s));
-        ok(cudaMemcpyAsync(&rows_crc, row_crc + max_blocks, 4, cudaMemcpyDeviceToHost, s));
+        ok(cudaMemcpyAsync(&total, total_bytes, 8, cudaMemcpyDeviceToHost, s));
+        ok(cudaMemcpyAsync(&raw_crc, block_crc + max_blocks, 4, cudaMemcpyDeviceToHost, s));
         ok(cudaMemcpyAsync(hadler.data(), adler, 16 * (size_t)height, cudaMemcpyDeviceToHost, s));
         ok(cudaStreamSynchronize(s));
     }
-    // file layout: signature, IHDR, IDAT {78 01, rows, Adler-32}, IEND
+    // file layout: signature, IHDR, IDAT {78 01, deflate block, Adler-32}, IEND
     const size_t idat_len = 2 + (size_t)total + 4;
     const size_t file_len = 8 + 25 + 8 + idat_len + 4 + 12;
     *out_len = file_len;
@@ -527,36 +702,39 @@ extern "C" VC_API int vc_encode_png(const uint8_t* d_rgba, int width, int height
         memcpy(id + 4, "IDAT", 4);
         id[8] = 0x78;
         id[9] = 0x01;
-        // the compressed rows go straight from HBM into the caller's buffer
-        ok(cudaMemcpyAsync(id + 10, packed, total, cudaMemcpyDeviceToHost, s));
+        // the deflate block goes straight from HBM into the caller's buffer
+        ok(cudaMemcpyAsync(id + 10, words, total, cudaMemcpyDeviceToHost, s));
         // Adler-32 of all filtered rows (per-row sums from the device)
         unsigned long long A = 1, B = 0;
         for (int y = 0; y < height; y++) {
-            B = (B + (n % 65521) * A + hadler[2 * y + 1] % 65521) % 65521;
+            B = (B + ((unsigned long long)n % 65521) * A + hadler[2 * y + 1] % 65521) % 65521;
             A = (A + hadler[2 * y] % 65521) % 65521;
         }
         uint8_t ad[4];
         put_be32(ad, (uint32_t)((B << 16) | A));
-        // CRC over "IDAT", the zlib header, the rows (device) and the Adler
-        // the device's raw CRC of the rows -> their PNG CRC, then chain
-        const uint32_t rows_std = rows_crc ^ shift_host(0xFFFFFFFFu, total) ^ 0xFFFFFFFFu;
+        // CRC over "IDAT", the zlib header, the block (device) and the Adler
+        const uint32_t block_std = raw_crc ^ shift_host(0xFFFFFFFFu, total) ^ 0xFFFFFFFFu;
         uint32_t c = crc32(id + 4, 6);
-        c = crc32_combine_host(c, rows_std, total);
+        c = crc32_combine_host(c, block_std, total);
         c = crc32(ad, 4, c);
         ok(cudaStreamSynchronize(s));
         memcpy(id + 10 + total, ad, 4);
         put_be32(id + 10 + total + 4, c);
-        uint8_t* ie = id + 10 + total + 8;
         const uint8_t iend[12] = {0, 0, 0, 0, 'I', 'E', 'N', 'D', 0xAE, 0x42, 0x60, 0x82};
-        memcpy(ie, iend, 12);
+        memcpy(id + 10 + total + 8, iend, 12);
     }
-    cudaFreeAsync(rowbuf, s);
-    cudaFreeAsync(row_bytes, s);
-    cudaFreeAsync(row_crc, s);
-    cudaFreeAsync(tables, s);
+    cudaFreeAsync(tokens, s);
+    cudaFreeAsync(ntok, s);
+    cudaFreeAsync(slice_bits, s);
+    cudaFreeAsync(row_bits, s);
+    cudaFreeAsync(hist, s);
     cudaFreeAsync(adler, s);
     cudaFreeAsync(offsets, s);
-    cudaFreeAsync(packed, s);
+    cudaFreeAsync(total_bytes, s);
+    cudaFreeAsync(words, s);
+    cudaFreeAsync(codes, s);
+    cudaFreeAsync(tables, s);
+    cudaFreeAsync(block_crc, s);
     if (rc != VC_OK) return rc;
     if (h_out != nullptr && h_cap < file_len) return VC_ERR_INVALID;
     return VC_OK;

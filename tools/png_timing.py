@@ -13,7 +13,7 @@ t0 = time.perf_counter()
 for i in range(20): png = egress.png_bytes(t)
 print("png_bytes(device tensor) ms", (time.perf_counter() - t0) / 20 * 1000, len(png))
 L = _native.load()
-cap = 64 + 1080 * ((1 + 3 * 1920) * 9 // 8 + 128)
+cap = 1024 + 1080 * ((1 + 3 * 1920) * 9 // 8 + 16)
 buf = ctypes.create_string_buffer(cap)
 n = ctypes.c_size_t(0)
 t0 = time.perf_counter()
