@@ -13,7 +13,7 @@
 //     matches: zero runs over background, repeating RGB along flat shading)
 //     into a token buffer and a shared symbol histogram;
 //   * code: the frame is ONE dynamic-Huffman deflate block.  The host turns
-//     the histogram into length-limited canonical codes (zlib-style) and
+//     the histogram into length-limited canonical codes (package-merge) and
 //     the block header; every thread then knows its bit count, a scan gives
 //     its bit offset, and all threads write their codes in parallel at those
 //     offsets (whole words from a register bit buffer, atomics only on the
@@ -440,62 +440,50 @@ void put_be32(uint8_t* o, uint32_t x) {
 }
 
 // ---- Huffman code construction (host) ---------------------------------
-// Huffman code lengths of the used symbols (two-queue construction over the
-// frequency-sorted leaves), limited to maxlen the way zlib does (trees.c
-// gen_bitlen: overflowing leaves go to maxlen, then the Kraft sum is
-// repaired by splitting shorter leaves); the longest codes go to the
-// rarest symbols.  A single used symbol gets length 1.
+// Optimal code lengths limited to maxlen: package-merge in its prefix form.
+// List j is merge(leaves, pairs of list j-1) by weight; the first 2m-2
+// items of list maxlen are selected, and a selected prefix of list j holds
+// p packages, which select the first 2p items of list j-1; every selected
+// leaf adds one to its symbol's length.  O(maxlen * m), no per-item symbol
+// sets.  A single used symbol gets length 1.
 std::vector<int> limited_lengths(const std::vector<unsigned long long>& freq, int maxlen) {
     const int n = (int)freq.size();
-    std::vector<int> len(n, 0), used;
+    std::vector<int> len(n, 0);
+    struct Item {
+        unsigned long long w;
+        int sym;  // >= 0 leaf, -1 package
+    };
+    std::vector<Item> leaves;
     for (int i = 0; i < n; i++)
-        if (freq[i]) used.push_back(i);
-    const int m = (int)used.size();
+        if (freq[i]) leaves.push_back({freq[i], i});
+    const int m = (int)leaves.size();
     if (m == 0) return len;
     if (m == 1) {
-        len[used[0]] = 1;
+        len[leaves[0].sym] = 1;
         return len;
     }
-    std::stable_sort(used.begin(), used.end(), [&](int x, int y) { return freq[x] < freq[y]; });
-    // nodes 0..m-1 leaves (ascending weight), m..2m-2 internal; parent links
-    std::vector<unsigned long long> w(2 * m - 1);
-    std::vector<int> parent(2 * m - 1, -1);
-    for (int i = 0; i < m; i++) w[i] = freq[used[i]];
-    int li = 0, ii = m, next = m;
-    auto take = [&]() {
-        if (li < m && (ii >= next || w[li] <= w[ii])) return li++;
-        return ii++;
-    };
-    while (next < 2 * m - 1) {
-        const int x = take(), y = take();
-        w[next] = w[x] + w[y];
-        parent[x] = parent[y] = next;
-        next++;
+    std::stable_sort(leaves.begin(), leaves.end(), [](const Item& a, const Item& b) { return a.w < b.w; });
+    std::vector<std::vector<Item>> lists(maxlen + 1);
+    lists[1] = leaves;
+    for (int j = 2; j <= maxlen; j++) {
+        const std::vector<Item>& prev = lists[j - 1];
+        std::vector<Item> pk;
+        pk.reserve(prev.size() / 2);
+        for (size_t i = 0; i + 1 < prev.size(); i += 2) pk.push_back({prev[i].w + prev[i + 1].w, -1});
+        std::vector<Item>& cur = lists[j];
+        cur.reserve(leaves.size() + pk.size());
+        std::merge(leaves.begin(), leaves.end(), pk.begin(), pk.end(), std::back_inserter(cur),
+                   [](const Item& a, const Item& b) { return a.w < b.w; });
     }
-    std::vector<int> depth(2 * m - 1, 0);
-    for (int i = 2 * m - 3; i >= 0; i--) depth[i] = depth[parent[i]] + 1;
-    std::vector<int> bl_count(64, 0);
-    int overflow = 0;
-    for (int i = 0; i < m; i++) {
-        int d = depth[i];
-        if (d > maxlen) {
-            d = maxlen;
-            overflow++;
+    size_t take = 2 * (size_t)m - 2;
+    for (int j = maxlen; j >= 1 && take > 0; j--) {
+        size_t npk = 0;
+        for (size_t i = 0; i < take && i < lists[j].size(); i++) {
+            if (lists[j][i].sym >= 0) len[lists[j][i].sym]++;
+            else npk++;
         }
-        bl_count[d]++;
+        take = 2 * npk;
     }
-    while (overflow > 0) {
-        int bits = maxlen - 1;
-        while (bl_count[bits] == 0) bits--;
-        bl_count[bits]--;
-        bl_count[bits + 1] += 2;
-        bl_count[maxlen]--;
-        overflow -= 2;
-    }
-    // lengths by count: the rarest symbols (front of `used`) get the longest
-    int k = 0;
-    for (int bits = maxlen; bits >= 1; bits--)
-        for (int c = 0; c < bl_count[bits]; c++) len[used[k++]] = bits;
     return len;
 }
 

@@ -413,6 +413,36 @@ def test_device_png_round_trip(wh):
     assert pos == len(png)
 
 
+@pytest.mark.parametrize("kind", ["skewed", "ramp", "noise", "flat"])
+def test_device_png_code_construction(kind):
+    """Symbol statistics that drive the shared dynamic Huffman code to its
+    corners: nearly all one symbol with rare outliers (length limiting at
+    15 bits), smooth ramps, uniform noise, a single colour (one literal)."""
+    import io
+
+    from PIL import Image
+
+    from paper_1609_01317_b200 import egress
+
+    H, W = 97, 211
+    rng = np.random.default_rng({"skewed": 1, "ramp": 2, "noise": 3, "flat": 4}[kind])
+    img = np.zeros((H, W, 4), np.uint8)
+    img[..., 3] = 255
+    if kind == "skewed":
+        m = rng.random((H, W)) < 0.002
+        img[m, :3] = rng.integers(0, 256, (int(m.sum()), 3))
+    elif kind == "ramp":
+        img[..., 0] = (np.arange(W)[None, :] * 255 // W).astype(np.uint8)
+        img[..., 1] = (np.arange(H)[:, None] * 255 // H).astype(np.uint8)
+    elif kind == "noise":
+        img[..., :3] = rng.integers(0, 256, (H, W, 3))
+    else:
+        img[..., :3] = 77
+    png = egress.png_bytes(img)
+    dec = np.asarray(Image.open(io.BytesIO(png)).convert("RGB"))
+    assert np.array_equal(dec, img[..., :3])
+
+
 def test_render_frame_png_matches_render_frame():
     import io
 
