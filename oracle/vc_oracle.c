@@ -10,12 +10,14 @@
  * reference kernel layer /root/reference/pkg/src/voxelcast/_kernels.py
  * (numba, fastmath off, no FMA contraction -- compile with
  * -ffp-contract=off).  Every function cites the reference lines it
- * follows.  The octree's empty-space segments are not restated: the oracle
- * is the brute-force renderer (render_frame(..., use_octree=False)), which
- * the reference guarantees is pixel-identical to the octree path
- * (pkg/tests/test_render.py:125-139).  The adaptive stride
- * (use_adaptive, _kernels.py:437-463) is restated over the reference's flat
- * octree arrays (built by oracle.build_octree_flat).
+ * follows.  By default the oracle is the brute-force renderer
+ * (render_frame(..., use_octree=False)), which the reference guarantees is
+ * pixel-identical to the octree path (pkg/tests/test_render.py:125-139);
+ * with use_octree set it marches the reference's merged octree segments
+ * (collect_segments, _kernels.py:267-342), which changes the sample count
+ * and, under use_adaptive, which samples exist.  The adaptive stride
+ * (use_adaptive, _kernels.py:437-463) and the segments are restated over the
+ * reference's flat octree arrays (built by oracle.build_octree_flat).
  *
  * Parity is pinned against golden fixtures produced by running the
  * reference itself (tests/golden/make_golden.py).

@@ -24,7 +24,10 @@
 //     over lattice samples t_enter + k*coarse that provably lie in cells
 //     whose 8 corners are all outside the threshold window, so the
 //     evaluated samples -- and the image -- are those of the brute-force
-//     march (the invariant of pkg/tests/test_render.py:125-139).
+//     march (the invariant of pkg/tests/test_render.py:125-139).  Only
+//     use_adaptive with use_octree replays the reference's octree-segment
+//     walk (firsthit_seg_kernel), because there the samples that exist
+//     decide the pixel.
 //   * the shading gradient comes either from the reference taps or from
 //     the packed float4 volume of Kernel 1 (interior only; the 1-voxel
 //     boundary band always uses the taps); the scalar field either from the
@@ -374,7 +377,7 @@ __device__ __forceinline__ int image_row(const vc_render_params& P, int lr) {
 // ray generation (_kernels.py:639-648) + box interval (:649); false = miss
 template <typename T>
 __device__ __forceinline__ bool start_ray(Ctx<T>& C, const vc_render_params& P, int px, int py,
-                                          RayState& R) {
+                                          RayState& R, double* t_exit_out = nullptr) {
     const double H = (double)P.height, W = (double)P.width;  // integers: never an all-ones significand
     const double v_ndc = dsub(1.0, ddiv_rcp(dmul(2.0, dadd((double)py, 0.5)), H, __drcp_rn(H)));
     const double u_ndc = dsub(ddiv_rcp(dmul(2.0, dadd((double)px, 0.5)), W, __drcp_rn(W)), 1.0);
@@ -393,6 +396,7 @@ __device__ __forceinline__ bool start_ray(Ctx<T>& C, const vc_render_params& P, 
     double t_enter, t_exit;
     if (!box_interval(C.rp.o, C.rp.d, P.clip_lo, P.clip_hi, t_enter, t_exit)) return false;
     R.t_enter = t_enter;
+    if (t_exit_out != nullptr) *t_exit_out = t_exit;
     R.lim = dadd(t_exit, 1e-12);
     R.base = t_enter;
     R.k = 0.0;
@@ -415,6 +419,35 @@ struct StrideArgs {
     double o[3], d[3], s[3];
     double detail_eps, coarse;
 };
+
+// _node_interval (_kernels.py:227-264) of box b of level L of the level grid
+__device__ __forceinline__ bool oct_node_interval(const OctDev& o, int L, const int b[3], const double ov3[3],
+                                                  const double d3[3], const double s3[3], double& tmin,
+                                                  double& tmax) {
+    tmin = -1e300;
+    tmax = 1e300;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        const int* iv = o.ivl + __ldg(o.ivl_off + 3 * L + a) + 2 * b[a];
+        const double lo = dmul((double)__ldg(iv), s3[a]);
+        const double hi = dmul((double)__ldg(iv + 1), s3[a]);
+        const double ov = ov3[a], d = d3[a];
+        if (d == 0.0) {
+            if (ov < lo || ov > hi) return false;
+        } else {
+            const double inv = ddiv(1.0, d);
+            double ta = dmul(dsub(lo, ov), inv), tb = dmul(dsub(hi, ov), inv);
+            if (ta > tb) {
+                const double sw = ta;
+                ta = tb;
+                tb = sw;
+            }
+            if (ta > tmin) tmin = ta;
+            if (tb < tmax) tmax = tb;
+        }
+    }
+    return !(tmin > tmax);
+}
 
 __device__ __noinline__ double adaptive_stride(const OctDev o, const StrideArgs A, double p0, double p1,
                                                double p2, double k, double t_enter) {
@@ -443,29 +476,8 @@ __device__ __noinline__ double adaptive_stride(const OctDev o, const StrideArgs 
     if (L == o.levels) return 1.0;  // unreachable for a well-formed tree
     const double smin = __ldg(o.srange + 2 * leaf), smax = __ldg(o.srange + 2 * leaf + 1);
     if (!(dsub(smax, smin) < A.detail_eps)) return 1.0;
-    // _node_interval of the leaf box
-    double tmin = -1e300, tmax = 1e300;
-#pragma unroll
-    for (int a = 0; a < 3; a++) {
-        const int* iv = o.ivl + __ldg(o.ivl_off + 3 * L + a) + 2 * b[a];
-        const double lo = dmul((double)__ldg(iv), A.s[a]);
-        const double hi = dmul((double)__ldg(iv + 1), A.s[a]);
-        const double ov = A.o[a], d = A.d[a];
-        if (d == 0.0) {
-            if (ov < lo || ov > hi) return 1.0;
-        } else {
-            const double inv = ddiv(1.0, d);
-            double ta = dmul(dsub(lo, ov), inv), tb = dmul(dsub(hi, ov), inv);
-            if (ta > tb) {
-                const double sw = ta;
-                ta = tb;
-                tb = sw;
-            }
-            if (ta > tmin) tmin = ta;
-            if (tb < tmax) tmax = tb;
-        }
-    }
-    if (tmin > tmax) return 1.0;
+    double tmin, tmax;
+    if (!oct_node_interval(o, L, b, A.o, A.d, A.s, tmin, tmax)) return 1.0;
     double step = (double)A.adapt_jump;
     const double kex = floor(ddiv(dsub(tmax, t_enter), A.coarse)) + 1.0;
     if (dsub(kex, k) < step) step = dsub(kex, k);
@@ -782,6 +794,222 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
     commit_counters(counters, 0, nsamp, nshade, nskip, nhit);
 }
 
+// use_adaptive with use_octree (raycast.py:494-499, _kernels.py:656): the reference's first
+// hit marches only the merged t-segments of the octree leaves whose padded
+// range meets the window (collect_segments, _kernels.py:267-342), restarting
+// the lattice index at each segment (k = max(k, floor((s0 - t_enter) /
+// coarse)), _kernels.py:402-410) and striding adaptively inside.  Since the
+// adaptive stride can step over in-window samples, which samples exist
+// decides the pixel, so this mode replays the walk exactly: the same
+// depth-first near-to-far traversal (children sorted by entry with the same
+// insertion sort, so ties pop in the same order) over the level-grid tree,
+// consumed lazily -- the next leaf is pulled when the lattice passes the
+// current segment end; a leaf that merges (a0 <= s1 + 1e-9) only extends it,
+// which is what the eager list would have held.  The reference's segment
+// buffer cap (raycast.py:499, 4096: further leaves overwrite the last end)
+// is honoured by draining the walk before marching the last segment.
+constexpr int SEG_CAP = 4096;
+constexpr int SEG_STACK = 1 + 7 * 17;  // depth-first stack bound for <= 17 levels
+
+struct SegWalk {
+    unsigned long long stack[SEG_STACK];
+    int sp;
+    double tray0, tray1;
+};
+
+__device__ __forceinline__ unsigned long long seg_node(int L, int bx, int by, int bz) {
+    return ((unsigned long long)L << 57) | ((unsigned long long)bz << 38) | ((unsigned long long)by << 19) |
+           (unsigned long long)bx;
+}
+
+// next emitted leaf interval [a0, b0] of the walk (false: walk finished)
+__device__ __noinline__ bool seg_next_leaf(const OctDev& o, SegWalk& W, const StrideArgs& A, double t_low,
+                                           double t_high, double& a0, double& b0) {
+    const unsigned M = (1u << 19) - 1u;
+    while (W.sp > 0) {
+        const unsigned long long node = W.stack[--W.sp];
+        const int L = (int)(node >> 57);
+        const int b[3] = {(int)(node & M), (int)((node >> 19) & M), (int)((node >> 38) & M)};
+        double ta, tb;
+        if (!oct_node_interval(o, L, b, A.o, A.d, A.s, ta, tb)) continue;
+        if (ta < W.tray0) ta = W.tray0;
+        if (tb > W.tray1) tb = W.tray1;
+        if (tb < ta) continue;
+        const long long box = __ldg(o.box_off + L) +
+                              ((long long)b[2] * __ldg(o.dims + 3 * L + 1) + b[1]) * __ldg(o.dims + 3 * L + 0) + b[0];
+        if (__ldg(o.state + box) == 2) {  // leaf
+            if (__ldg(o.srange + 2 * box) <= t_high && __ldg(o.srange + 2 * box + 1) >= t_low) {
+                a0 = ta;
+                b0 = tb;
+                return true;
+            }
+            continue;
+        }
+        // children: the next level's boxes inside this one, z-major like the
+        // reference's construction order (octree.py:97-105)
+        const int stride_map = A.nx + A.ny + A.nz;
+        const int* m = o.amap + (size_t)(L + 1) * stride_map;
+        int c0[3], cn[3];
+        const int axoff[3] = {0, A.nx, A.nx + A.ny};
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            const int* iv = o.ivl + __ldg(o.ivl_off + 3 * L + a) + 2 * b[a];
+            const int lo = __ldg(iv), hi = __ldg(iv + 1);
+            c0[a] = __ldg(m + axoff[a] + lo);
+            cn[a] = hi - lo >= 2 ? 2 : 1;
+        }
+        double ct[8];
+        unsigned long long ci[8];
+        int cnt = 0;
+        for (int cz = 0; cz < cn[2]; cz++)
+            for (int cy = 0; cy < cn[1]; cy++)
+                for (int cx = 0; cx < cn[0]; cx++) {
+                    const int cb[3] = {c0[0] + cx, c0[1] + cy, c0[2] + cz};
+                    double ca, cbb;
+                    if (!oct_node_interval(o, L + 1, cb, A.o, A.d, A.s, ca, cbb) || cbb < W.tray0 ||
+                        ca > W.tray1)
+                        continue;
+                    ct[cnt] = ca;
+                    ci[cnt] = seg_node(L + 1, cb[0], cb[1], cb[2]);
+                    cnt++;
+                }
+        for (int a = 1; a < cnt; a++) {  // farthest entry first: the nearest pops first
+            const double tv = ct[a];
+            const unsigned long long iv = ci[a];
+            int j = a - 1;
+            while (j >= 0 && ct[j] < tv) {
+                ct[j + 1] = ct[j];
+                ci[j + 1] = ci[j];
+                j--;
+            }
+            ct[j + 1] = tv;
+            ci[j + 1] = iv;
+        }
+        for (int a = 0; a < cnt && W.sp < SEG_STACK; a++) W.stack[W.sp++] = ci[a];
+    }
+    return false;
+}
+
+// first lattice sample in the window over the segments (R.found / R.t_hit)
+template <typename T, int INTERP>
+__device__ void seg_first_hit(const Ctx<T>& C, const vc_render_params& P, const OctDev& o, RayState& R,
+                              double t_exit, unsigned& nsamp) {
+    StrideArgs A;
+    A.nx = C.v.nx;
+    A.ny = C.v.ny;
+    A.nz = C.v.nz;
+    A.adapt_jump = P.adapt_jump;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        A.o[a] = C.rp.o[a];
+        A.d[a] = C.rp.d[a];
+        A.s[a] = C.rp.s[a];
+    }
+    A.detail_eps = P.detail_eps;
+    A.coarse = P.coarse;
+    SegWalk W;
+    W.sp = 0;
+    W.stack[W.sp++] = seg_node(0, 0, 0, 0);
+    W.tray0 = R.t_enter;
+    W.tray1 = t_exit;
+    int nseg = 0;
+    double s0, s1;
+    bool pending = seg_next_leaf(o, W, A, P.t_low, P.t_high, s0, s1);
+    while (pending) {
+        pending = false;
+        if (++nseg == SEG_CAP) {  // the reference's last buffer slot takes every later leaf
+            double a0, b0;
+            while (seg_next_leaf(o, W, A, P.t_low, P.t_high, a0, b0)) {
+                if (a0 <= dadd(s1, 1e-9)) {
+                    if (b0 > s1) s1 = b0;
+                } else {
+                    s1 = b0;
+                }
+            }
+        }
+        const double kk = floor(ddiv(dsub(s0, R.t_enter), P.coarse));
+        if (kk > R.k) R.k = kk;
+        for (;;) {
+            const double t = dadd(R.t_enter, dmul(R.k, P.coarse));
+            if (t > R.lim) return;  // every later segment starts at or after t
+            if (t > dadd(s1 > t_exit ? t_exit : s1, 1e-12)) {
+                double a0, b0;
+                if (nseg == SEG_CAP || !seg_next_leaf(o, W, A, P.t_low, P.t_high, a0, b0)) return;
+                if (a0 <= dadd(s1, 1e-9)) {  // merges into the current segment
+                    if (b0 > s1) s1 = b0;
+                    continue;
+                }
+                s0 = a0;
+                s1 = b0;
+                pending = true;
+                break;
+            }
+            double p[3];
+            C.rp.at(t, p);
+            nsamp++;
+            if (window_at<T, INTERP>(C, P, p)) {
+                R.found = true;
+                R.t_hit = t;
+                return;
+            }
+            R.k += P.use_adaptive ? adaptive_stride(o, A, p[0], p[1], p[2], R.k, R.t_enter) : 1.0;
+        }
+    }
+}
+
+// Kernel A for the segment mode: one ray per thread (the mode is off the
+// hot path), same work-item tiling, hit queue and counters as Kernel A.
+template <typename T, int INTERP>
+__global__ void __launch_bounds__(128) firsthit_seg_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
+                                                           RayPos rp0, PixelSink sink, int local_rows,
+                                                           unsigned long long* counters, FrameWork* work,
+                                                           HitEntry* __restrict__ hits, OctDev oct) {
+    const int tiles_x = (P.width + 7) >> 3;
+    const unsigned total = (unsigned)tiles_x * (unsigned)((local_rows + 3) >> 2) * 32u;
+    const unsigned w = blockIdx.x * 128u + threadIdx.x;
+    Ctx<T> C;
+    init_ctx(C, P, vol, nullptr, rp0, nullptr, 0, 0, 0, TexArgs{});
+    unsigned nsamp = 0, nhit = 0;
+    RayState R;
+    R.found = false;
+    int px = 0, lr = 0;
+    if (w < total) {
+        const unsigned tile = w >> 5, r = w & 31u;
+        px = (int)(tile % (unsigned)tiles_x) * 8 + (int)(r & 7u);
+        lr = (int)(tile / (unsigned)tiles_x) * 4 + (int)(r >> 3);
+        if (px < P.width && lr < local_rows) {
+            double t_exit = 0.0;
+            if (start_ray(C, P, px, image_row(P, lr), R, &t_exit)) {
+                nhit++;
+                seg_first_hit<T, INTERP>(C, P, oct, R, t_exit, nsamp);
+                if (!R.found) put_pixel(sink, P, lr, px, bg_pixel(P));
+            } else {
+                put_pixel(sink, P, lr, px, bg_pixel(P));
+            }
+        }
+    }
+    const bool hit = R.found;
+    double t_star = 0.0;
+    if (hit) t_star = refine_hit<T, INTERP>(C, P, R, R.t_hit, nsamp);
+    const unsigned q = warp_ticket(&work->hits, hit);
+    if (hit) {
+        HitEntry e;
+        e.t_star = t_star;
+        e.lim = R.lim;
+        e.d[0] = C.rp.d[0];
+        e.d[1] = C.rp.d[1];
+        e.d[2] = C.rp.d[2];
+        e.ib[0] = C.sk.ib[0];
+        e.ib[1] = C.sk.ib[1];
+        e.ib[2] = C.sk.ib[2];
+        e.t_enter = R.t_enter;
+        e.lr = lr;
+        e.px = px;
+        hits[q] = e;
+    }
+    commit_counters(counters, 0, nsamp, 0, 0, nhit);
+}
+
 // Kernel B -- shade + composite (wavefront stage 2).  Persistent CTAs pull
 // first hits from the queue, regenerate the ray, shade at t_star and, in
 // composited mode, keep marching t_star + m*coarse and shading in-window
@@ -906,9 +1134,18 @@ static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
     tex.hi = (float)L.p->t_high;
     if ((double)tex.hi > L.p->t_high) tex.hi = std::nextafter(tex.hi, -INFINITY);
     if (L.ev[0]) cudaEventRecord(L.ev[0], stream);
-    firsthit_kernel<T, INTERP><<<persistent_blocks(firsthit_kernel<T, INTERP>, (tiles + 3) / 4), 128, 0, stream>>>(
-        *L.p, vol, L.rp, L.occ, L.mx, L.my, L.skip_on, sink, L.local_rows,
-        reinterpret_cast<unsigned long long*>(L.counters), fw, hits, L.oct, tex);
+    // use_adaptive + use_octree: the octree-segment first hit (exact reference walk)
+    const bool seg = INTERP != VC_TEX && L.p->use_adaptive && L.p->skip_empty;
+    if (seg) {
+        if constexpr (INTERP != VC_TEX)
+            firsthit_seg_kernel<T, INTERP><<<(unsigned)((tiles * 32 + 127) / 128), 128, 0, stream>>>(
+                *L.p, vol, L.rp, sink, L.local_rows, reinterpret_cast<unsigned long long*>(L.counters), fw,
+                hits, L.oct);
+    } else {
+        firsthit_kernel<T, INTERP><<<persistent_blocks(firsthit_kernel<T, INTERP>, (tiles + 3) / 4), 128, 0, stream>>>(
+            *L.p, vol, L.rp, L.occ, L.mx, L.my, L.skip_on, sink, L.local_rows,
+            reinterpret_cast<unsigned long long*>(L.counters), fw, hits, L.oct, tex);
+    }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (L.ev[1]) cudaEventRecord(L.ev[1], stream);

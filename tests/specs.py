@@ -67,5 +67,5 @@ def spec_of(scene_settings) -> dict:
                      "refine_iters": st.refine_iters, "background": list(st.background),
                      "use_adaptive": st.use_adaptive, "adaptive_factor": st.adaptive_factor,
                      "detail_epsilon": st.detail_epsilon, "octree_min_block": st.octree_min_block,
-                     "octree_max_depth": st.octree_max_depth},
+                     "octree_max_depth": st.octree_max_depth, "use_octree": st.use_octree},
     }

@@ -48,6 +48,24 @@ def test_frame_bit_exact_with_empty_space_skipping(golden, name):
         assert fb.sample_count <= want_count
 
 
+def _reference_octree_frames():
+    from tests.conftest import GOLDEN, Golden
+
+    return [e["name"] for e in Golden(GOLDEN).frames() if e["spec"].get("settings", {}).get("use_octree")]
+
+
+@pytest.mark.parametrize("name", _reference_octree_frames())
+def test_frame_octree_segments_match_reference_count(golden, name):
+    """Frames the reference rendered with use_octree=True (adaptive stride
+    restarted at its octree segments): the device's segment walk gives the
+    reference's pixels and the reference's own sample count."""
+    arr, spacing, spec, want_px, want_count = golden.frame(name)
+    vol = product_volume(arr, spacing)
+    fb = vc.render_frame(vol, product_scene(spec), product_settings(spec, use_octree=True))
+    assert np.array_equal(fb.pixels, want_px), f"max|d|={maxdiff(fb.pixels, want_px)}"
+    assert fb.sample_count == want_count
+
+
 @pytest.mark.parametrize("name", frame_names())
 def test_frame_gradient_volume_within_one_lsb(golden, name):
     arr, spacing, spec, want_px, _ = golden.frame(name)
@@ -322,11 +340,14 @@ def test_adaptive_stride_vs_oracle(mode):
         assert maxdiff(fb2.pixels, want) <= 1
         # use_octree=True as the reference runs it (segment restarts,
         # restated in the oracle and pinned to the reference's counts): the
-        # same pixels; only the sample count differs
+        # device replays the same walk -- same pixels, same count
         st3 = replace(st2, use_octree=True)
-        want3, _ = oracle.render(vol.as_array(), vol.spacing, spec_of((sc, st3)), octree=True)
+        want3, want3_count = oracle.render(vol.as_array(), vol.spacing, spec_of((sc, st3)), octree=True)
         fb3 = vc.render_frame(vol, sc, st3)
         assert np.array_equal(fb3.pixels, want3)
+        assert fb3.sample_count == want3_count
+        fb4 = vc.render_frame(vol, sc, replace(st3, gradient_source="volume"))
+        assert maxdiff(fb4.pixels, want3) <= 1
 
 
 @pytest.mark.parametrize("shape", [(1, 8, 8), (8, 1, 8), (2, 2, 2), (3, 17, 5), (1, 1, 1)])

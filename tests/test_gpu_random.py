@@ -96,7 +96,8 @@ def test_random_scene_vs_oracle(volumes, i):
 @pytest.mark.parametrize("i", range(32))
 def test_random_adaptive_scene_vs_oracle(volumes, i):
     """use_adaptive on the same kind of random scenes (random stride factor,
-    detail epsilon, octree block size): bit-exact, counts included."""
+    detail epsilon, octree block size), with and without the octree-segment
+    walk: bit-exact, counts included."""
     rng = np.random.default_rng(5000 + i)
     name = ["ct", "noise", "ml"][i % 3]
     vol, sc, st = _scene(rng, volumes[name], name)
@@ -104,7 +105,11 @@ def test_random_adaptive_scene_vs_oracle(volumes, i):
     st = replace(st, use_adaptive=True, use_octree=False, adaptive_factor=int(rng.integers(1, 9)),
                  detail_epsilon=None if rng.random() < 0.3 else float(rng.uniform(0.001, 0.3)) * vmax,
                  octree_min_block=int(rng.choice([2, 4, 8])))
-    want, want_count = oracle.render(vol.as_array(), vol.spacing, spec_of((sc, st)), threads=8)
+    # the reference's default use_octree=True restarts the stride at its
+    # octree segments: odd scenes run that walk
+    st = replace(st, use_octree=bool(i % 2))
+    want, want_count = oracle.render(vol.as_array(), vol.spacing, spec_of((sc, st)), threads=8,
+                                     octree=True)
     fb = vc.render_frame(vol, sc, st)
     d = np.abs(fb.pixels.astype(int) - want.astype(int))
     assert d.max() == 0, f"{int((d > 0).any(axis=2).sum())} px differ, max {int(d.max())}"
