@@ -189,12 +189,12 @@ def cpu_sample_fps(vol, frame, first_frame: int, target_s: float, threads: int):
     arr = vol.as_array()
     sc, st = frame(first_frame)
     H = st.height
-    nb = 8  # rows per band
+    nb = max(8, 2 * threads)  # rows per call: every host thread gets rows (the oracle deals them out)
     # estimate with a small sample, then size the real sample to target_s
     done_rows = 0
     spent = 0.0
     bands_used = 0
-    stride = 16
+    stride = max(1, (H // nb) // 8)  # ~8 bands spread over the image per pass
     order = list(range(0, H // nb, stride))
     f = first_frame
     t_start = time.perf_counter()

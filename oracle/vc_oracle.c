@@ -737,19 +737,24 @@ void vco_grad_volume(const void *data, int dtype, int nx, int ny, int nz, int op
 }
 
 /* Whole frame (or rows [y0, y1)), work split in bands of `band` rows
- * handed round-robin to `threads` workers, like raycast.py:476-505.
+ * (raycast.py:476-505 hands 16-row bands to a thread pool); here each
+ * worker pulls the next band from a shared counter, so every host thread
+ * stays busy down to single-row bands and small row samples.
  * Output rows outside [y0, y1) are untouched. */
 typedef struct {
     const vco_vol *v;
     const vco_params *P;
     uint8_t *out;
-    int y0, y1, band, tid, nthreads;
+    int y0, y1, band;
+    int *next;
     int64_t counter;
 } render_job;
 
 static void *render_worker(void *arg) {
     render_job *J = (render_job *)arg;
-    for (int b = J->y0 + J->tid * J->band; b < J->y1; b += J->nthreads * J->band) {
+    for (;;) {
+        int b = __atomic_fetch_add(J->next, J->band, __ATOMIC_RELAXED);
+        if (b >= J->y1) break;
         int e = b + J->band;
         if (e > J->y1) e = J->y1;
         render_rows(J->v, J->P, b, e, J->out, &J->counter);
@@ -762,10 +767,16 @@ int64_t vco_render(const void *data, int dtype, int nx, int ny, int nz, const vc
     vco_vol v = {data, dtype, nx, ny, nz};
     if (threads < 1) threads = 1;
     if (threads > 256) threads = 256;
+    /* bands of up to 4 rows, at least two per thread when the range allows */
+    int band = (y1 - y0) / (2 * threads);
+    if (band > 4) band = 4;
+    if (band < 1) band = 1;
+    if (threads > y1 - y0) threads = y1 - y0 > 0 ? y1 - y0 : 1;
+    int next = y0;
     pthread_t th[256];
     render_job jobs[256];
     for (int t = 0; t < threads; t++) {
-        jobs[t] = (render_job){&v, P, out, y0, y1, 4, t, threads, 0};
+        jobs[t] = (render_job){&v, P, out, y0, y1, band, &next, 0};
         pthread_create(&th[t], NULL, render_worker, &jobs[t]);
     }
     int64_t total = 0;
