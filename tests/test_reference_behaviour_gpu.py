@@ -4,8 +4,8 @@ the device through the C ABI).
 
 Sources, one section each: pkg/tests/test_render.py,
 pkg/tests/test_gradients.py, pkg/tests/test_raycast_pipeline.py,
-test_raycast_geometry.py (the device-backed helpers) and the on-path
-guarantees of test_acceptance.py.  The assertions and tolerances are the
+test_raycast_geometry.py (the device-backed helpers), the sampler half of
+test_volume.py and the on-path guarantees of test_acceptance.py.  The assertions and tolerances are the
 reference's; the fixtures and structure are this suite's."""
 
 from __future__ import annotations
@@ -595,3 +595,80 @@ def test_default_size_frame_independent_of_workers():
     sc = vc.default_scene(vol)
     frames = [vc.render_frame(vol, sc, vc.RenderSettings(), workers=n).pixels for n in (1, 2, 16)]
     assert np.array_equal(frames[0], frames[1]) and np.array_equal(frames[0], frames[2])
+
+
+# ---------------------------------------------------- test_volume.py: the sampler
+
+TRI, NEAR, LIN = vc.InterpolationMode.TRILINEAR, vc.InterpolationMode.NEAREST, vc.InterpolationMode.LINEAR
+
+
+@pytest.fixture(scope="module")
+def noise16_ref():
+    """The reference conftest's noise volume (seed 99)."""
+    r = np.random.default_rng(99)
+    return vc.Volume.from_array(r.integers(0, 4096, size=(16, 16, 16), dtype=np.uint16))
+
+
+def _corner_sum(arr, x, y, z):
+    i, j, k = int(math.floor(x)), int(math.floor(y)), int(math.floor(z))
+    fx, fy, fz = x - i, y - j, z - k
+    return sum(float(arr[k + c, j + b, i + a]) * (fx if a else 1 - fx) * (fy if b else 1 - fy) * (fz if c else 1 - fz)
+               for c in (0, 1) for b in (0, 1) for a in (0, 1))
+
+
+def test_trilinear_corner_sum_lattice_and_affine(noise16_ref):
+    """test_volume.py:37-62"""
+    arr = noise16_ref.as_array()
+    rng = np.random.default_rng(20240817)
+    for p in rng.uniform(0.0, 14.999, size=(300, 3)):
+        assert vc.sample(noise16_ref, p, TRI) == pytest.approx(_corner_sum(arr, *p), rel=1e-12, abs=1e-9)
+    for i, j, k in rng.integers(0, 16, size=(200, 3)):
+        assert vc.sample(noise16_ref, (i, j, k), TRI) == float(arr[k, j, i])
+    zi, yi, xi = np.meshgrid(np.arange(12), np.arange(12), np.arange(12), indexing="ij")
+    affine = vc.Volume.from_array((7 + 2 * xi + 3 * yi + 5 * zi).astype(np.uint16))
+    for x, y, z in rng.uniform(0, 11, size=(200, 3)):
+        assert vc.sample(affine, (x, y, z)) == pytest.approx(7 + 2 * x + 3 * y + 5 * z, rel=1e-9)
+
+
+def test_last_lattice_plane_interpolates(noise16_ref):
+    """test_volume.py:65-70: x = n-1 uses the last cell."""
+    want = _corner_sum(noise16_ref.as_array(), 14.9999999999, 7.2, 3.8)
+    assert vc.sample(noise16_ref, (15.0, 7.2, 3.8)) == pytest.approx(want, abs=1e-6)
+
+
+def test_nearest_rounding(noise16_ref):
+    """test_volume.py:73-86: halves round away from zero."""
+    arr = noise16_ref.as_array()
+    assert vc.sample(noise16_ref, (1.5, 2.0, 3.0), NEAR) == float(arr[3, 2, 2])
+    assert vc.sample(noise16_ref, (1.49, 2.0, 3.0), NEAR) == float(arr[3, 2, 1])
+    assert vc.sample(noise16_ref, (7.5, 7.5, 7.5), NEAR) == float(arr[8, 8, 8])
+    rng = np.random.default_rng(2)
+    for p in rng.uniform(0, 15, size=(200, 3)):
+        i, j, k = (int(math.floor(c + 0.5)) for c in p)
+        assert vc.sample(noise16_ref, p, NEAR) == float(arr[k, j, i])
+
+
+def test_linear_mode(noise16_ref):
+    """test_volume.py:89-113: interpolate along the axis farthest from
+    its lattice plane (ties: x, then y), round the others; equals trilinear
+    on the lattice."""
+    arr = noise16_ref.as_array()
+    assert vc.sample(noise16_ref, (2.3, 1.04, 3.96), LIN) == \
+        pytest.approx(0.7 * float(arr[4, 1, 2]) + 0.3 * float(arr[4, 1, 3]), rel=1e-12)
+    assert vc.sample(noise16_ref, (5.02, 9.01, 6.6), LIN) == \
+        pytest.approx(0.4 * float(arr[6, 9, 5]) + 0.6 * float(arr[7, 9, 5]), rel=1e-12)
+    assert vc.sample(noise16_ref, (1.5, 2.5, 3.5), LIN) == \
+        pytest.approx(0.5 * float(arr[4, 3, 1]) + 0.5 * float(arr[4, 3, 2]), rel=1e-12)
+    rng = np.random.default_rng(3)
+    for p in rng.integers(0, 16, size=(100, 3)).astype(float):
+        assert vc.sample(noise16_ref, p, LIN) == vc.sample(noise16_ref, p, TRI)
+
+
+def test_outside_reads_zero_and_non_finite_rejected(noise16_ref):
+    """test_volume.py:116-128"""
+    for mode in vc.InterpolationMode:
+        for p in ((-0.01, 5, 5), (5, 15.01, 5), (5, 5, -3.0)):
+            assert vc.sample(noise16_ref, p, mode) == 0.0
+    for bad in ((np.nan, 1, 1), (np.inf, 1, 1)):
+        with pytest.raises(ValueError):
+            vc.sample(noise16_ref, bad)
