@@ -212,9 +212,53 @@ __device__ __forceinline__ double w_to_double(float w) {
     }
 }
 
-template <typename T>
-__device__ __forceinline__ void grad_from_volume(const float4* __restrict__ G, int nx, int ny,
-                                                 const double p[3], float g[3], double& value) {
+// The suspect case of grad_from_volume, out of line (the corners are
+// re-read from L1 rather than kept live on the hot path): the same corners
+// re-interpolated in float64 -- exact inputs for CD / Sobel on integer
+// grids, so only 2^-53 M rounding remains; for ZH and float grids the
+// storage error 2^-24 M stays and |g| >= 1e-4 M is still required.
+// .w = 0 when the reference taps are needed after all (that, or the
+// EPS_GRADIENT band |g| < 2e-8).
+template <typename T, int OP>
+__device__ __noinline__ float4 gv_refine(const float4* __restrict__ b, uint32_t sy, uint32_t sz, double fx,
+                                         double fy, double fz, float M) {
+    const float4 c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + sy), c110 = __ldg(b + sy + 1);
+    const float4 c001 = __ldg(b + sz), c101 = __ldg(b + sz + 1), c011 = __ldg(b + sz + sy),
+                 c111 = __ldg(b + sz + sy + 1);
+    double h[3];
+#define VC_TRID(comp)                                                                                        \
+    lerp(lerp(lerp((double)c000.comp, (double)c100.comp, fx), lerp((double)c010.comp, (double)c110.comp, fx), \
+              fy),                                                                                           \
+         lerp(lerp((double)c001.comp, (double)c101.comp, fx), lerp((double)c011.comp, (double)c111.comp, fx), \
+              fy),                                                                                           \
+         fz)
+    h[0] = VC_TRID(x);
+    h[1] = VC_TRID(y);
+    h[2] = VC_TRID(z);
+#undef VC_TRID
+    const double h2 = dadd(dadd(dmul(h[0], h[0]), dmul(h[1], h[1])), dmul(h[2], h[2]));
+    constexpr bool exact_corners = std::is_integral<T>::value && OP != VC_OP_ZUCKER_HUMMEL;
+    const bool ok = !(h2 < 4e-16 || (!exact_corners && h2 < 1e-8 * ((double)M * (double)M)));
+    return make_float4((float)h[0], (float)h[1], (float)h[2], ok ? 1.0f : 0.0f);
+}
+
+// Trilinear interpolation of the packed gradient volume at an interior point
+// p: value (float64, exact) and the gradient for the diffuse term, in
+// float32.  Returns whether that gradient is suspect; `cell` and `M` feed
+// gv_refine then.
+//
+// The float32 gradient's absolute error is at most about 13 * 2^-24 * M
+// per component (M = largest corner component: the float32 storage of
+// irrational / float corners, then three lerp levels each rounding b - a,
+// the fraction and the fma), so its direction is good to the 1/255 bar
+// whenever |g| >= 1e-3 M.  Below that the corners cancel (a zero crossing
+// of the gradient field; ~0.08% of the C3 shades) and the sample is
+// suspect, as is one near the reference's EPS_GRADIENT cutoff (|g| < 2e-8
+// with nonzero corners), where the zero-normal decision could differ.
+template <typename T, int OP>
+__device__ __forceinline__ bool grad_from_volume(const float4* __restrict__ G, int nx, int ny,
+                                                 const double p[3], float g[3], double& value,
+                                                 const float4*& cell, float& M) {
     double fx, fy, fz;
     double r;  // interior point: no clamping
     const int i0 = floor_pos(p[0], r);
@@ -225,6 +269,7 @@ __device__ __forceinline__ void grad_from_volume(const float4* __restrict__ G, i
     fz = dsub(p[2], r);
     const uint32_t sy = (uint32_t)nx, sz = (uint32_t)nx * (uint32_t)ny;
     const float4* b = G + (((uint32_t)k0 * (uint32_t)ny + (uint32_t)j0) * (uint32_t)nx + (uint32_t)i0);
+    cell = b;
     const float4 c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + sy), c110 = __ldg(b + sy + 1);
     const float4 c001 = __ldg(b + sz), c101 = __ldg(b + sz + 1), c011 = __ldg(b + sz + sy),
                  c111 = __ldg(b + sz + sy + 1);
@@ -242,6 +287,12 @@ __device__ __forceinline__ void grad_from_volume(const float4* __restrict__ G, i
     value = lerp(lerp(lerp(VC_W(c000), VC_W(c100), fx), lerp(VC_W(c010), VC_W(c110), fx), fy),
                  lerp(lerp(VC_W(c001), VC_W(c101), fx), lerp(VC_W(c011), VC_W(c111), fx), fy), fz);
 #undef VC_W
+#define VC_AM(c) fmaxf(fabsf(c.x), fmaxf(fabsf(c.y), fabsf(c.z)))
+    M = fmaxf(fmaxf(fmaxf(VC_AM(c000), VC_AM(c100)), fmaxf(VC_AM(c010), VC_AM(c110))),
+              fmaxf(fmaxf(VC_AM(c001), VC_AM(c101)), fmaxf(VC_AM(c011), VC_AM(c111))));
+#undef VC_AM
+    const float g2 = fmaf(g[0], g[0], fmaf(g[1], g[1], g[2] * g[2]));
+    return g2 < 1e-6f * M * M || (g2 < 4e-16f && M > 0.0f);
 }
 
 #ifdef VC_DEBUG_TAPS
@@ -290,10 +341,14 @@ __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_pa
     double val, illum = 0.0;
     const bool interior = p[0] >= 1.0 && p[0] <= dsub(C.v.mx, 1.0) && p[1] >= 1.0 &&
                           p[1] <= dsub(C.v.my, 1.0) && p[2] >= 1.0 && p[2] <= dsub(C.v.mz, 1.0);
-    if (GV && interior) {
+    bool taps = !(GV && interior);
+    if (!taps) {
         // diffuse term in float32 from the stored float32 gradient:
         // illum = dot(L, -g) / (|L| |g|), 0 for |g| <= EPS_GRADIENT or |L| = 0
         float g[3];
+        bool suspect = false;
+        const float4* cell = nullptr;
+        float M = 0.0f;
         if (INTERP == VC_TEX) {  // one filtered float4 fetch: gradient + value
             const float4 q = tex3D<float4>(C.tx.g, __double2float_rn(p[0]) + 0.5f,
                                            __double2float_rn(p[1]) + 0.5f, __double2float_rn(p[2]) + 0.5f);
@@ -303,7 +358,7 @@ __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_pa
             val = (double)q.w;
         } else {
             double gv;
-            grad_from_volume<T>(C.grad, C.v.nx, C.v.ny, p, g, gv);
+            suspect = grad_from_volume<T, OP>(C.grad, C.v.nx, C.v.ny, p, g, gv, cell, M);
             val = (INTERP == VC_TRILINEAR) ? gv : sample_any<T, INTERP>(C.v, p[0], p[1], p[2]);
         }
         const float lx = (float)dsub(P.light_pos[0], wx);
@@ -315,7 +370,31 @@ __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_pa
             const float d = -fmaf(lx, g[0], fmaf(ly, g[1], lz * g[2]));
             illum = (double)(d * rsqrtf(g2) * rsqrtf(l2));
         }
-    } else {
+        if constexpr (INTERP != VC_TEX) {
+            if (__builtin_expect(suspect, 0)) {  // cancelling corners (grad_from_volume)
+                const uint32_t sy = (uint32_t)C.v.nx, sz = (uint32_t)C.v.nx * (uint32_t)C.v.ny;
+                double r;
+                floor_pos(p[0], r);
+                const double fx = dsub(p[0], r);
+                floor_pos(p[1], r);
+                const double fy = dsub(p[1], r);
+                floor_pos(p[2], r);
+                const double fz = dsub(p[2], r);
+                const float4 h = gv_refine<T, OP>(cell, sy, sz, fx, fy, fz, M);
+                if (h.w == 0.0f) {
+                    taps = true;
+                } else {
+                    illum = 0.0;
+                    const float h2 = fmaf(h.x, h.x, fmaf(h.y, h.y, h.z * h.z));
+                    if (h2 > 1e-16f && l2 > 0.0f) {
+                        const float d = -fmaf(lx, h.x, fmaf(ly, h.y, lz * h.z));
+                        illum = (double)(d * rsqrtf(h2) * rsqrtf(l2));
+                    }
+                }
+            }
+        }
+    }
+    if (taps) {
 #ifdef VC_DEBUG_TAPS
         if (GV) atomicAdd(&g_debug_taps, 1u);
 #endif

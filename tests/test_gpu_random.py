@@ -114,3 +114,16 @@ def test_random_adaptive_scene_vs_oracle(volumes, i):
     d = np.abs(fb.pixels.astype(int) - want.astype(int))
     assert d.max() == 0, f"{int((d > 0).any(axis=2).sum())} px differ, max {int(d.max())}"
     assert fb.sample_count == want_count
+
+
+def test_gradient_volume_cancellation_regression(volumes):
+    """A scene from the 10 000-scene sweep (tools/parity_sweep.py, seed
+    206744: f32 grid, nearest interpolation, CD) where the gradient field
+    crosses zero at a shaded sample: the float32 interpolated gradient lost
+    its direction (32 LSB off) until near-cancelling corners were routed to
+    the exact taps."""
+    rng = np.random.default_rng(206744)
+    vol, sc, st = _scene(rng, volumes["ct"], "ct")
+    want, _ = oracle.render(vol.as_array(), vol.spacing, spec_of((sc, st)), threads=8)
+    fb = vc.render_frame(vol, sc, replace(st, gradient_source="volume"))
+    assert int(np.abs(fb.pixels.astype(int) - want.astype(int)).max()) <= 1
