@@ -496,13 +496,14 @@ __device__ __forceinline__ bool start_ray(Ctx<T>& C, const vc_render_params& P, 
 struct StrideArgs {
     int nx, ny, nz, adapt_jump;
     double o[3], d[3], s[3];
+    double inv[3];  // 1.0 / d (the reference's per-call value; computed once per ray)
     double detail_eps, coarse;
 };
 
 // _node_interval (_kernels.py:227-264) of box b of level L of the level grid
 __device__ __forceinline__ bool oct_node_interval(const OctDev& o, int L, const int b[3], const double ov3[3],
-                                                  const double d3[3], const double s3[3], double& tmin,
-                                                  double& tmax) {
+                                                  const double d3[3], const double inv3[3], const double s3[3],
+                                                  double& tmin, double& tmax) {
     tmin = -1e300;
     tmax = 1e300;
 #pragma unroll
@@ -514,7 +515,7 @@ __device__ __forceinline__ bool oct_node_interval(const OctDev& o, int L, const 
         if (d == 0.0) {
             if (ov < lo || ov > hi) return false;
         } else {
-            const double inv = ddiv(1.0, d);
+            const double inv = inv3[a];
             double ta = dmul(dsub(lo, ov), inv), tb = dmul(dsub(hi, ov), inv);
             if (ta > tb) {
                 const double sw = ta;
@@ -556,7 +557,7 @@ __device__ __noinline__ double adaptive_stride(const OctDev o, const StrideArgs 
     const double smin = __ldg(o.srange + 2 * leaf), smax = __ldg(o.srange + 2 * leaf + 1);
     if (!(dsub(smax, smin) < A.detail_eps)) return 1.0;
     double tmin, tmax;
-    if (!oct_node_interval(o, L, b, A.o, A.d, A.s, tmin, tmax)) return 1.0;
+    if (!oct_node_interval(o, L, b, A.o, A.d, A.inv, A.s, tmin, tmax)) return 1.0;
     double step = (double)A.adapt_jump;
     const double kex = floor(ddiv(dsub(tmax, t_enter), A.coarse)) + 1.0;
     if (dsub(kex, k) < step) step = dsub(kex, k);
@@ -590,6 +591,7 @@ __device__ __forceinline__ void march_step(const Ctx<T>& C, const vc_render_para
             A.o[a] = C.rp.o[a];
             A.d[a] = C.rp.d[a];
             A.s[a] = C.rp.s[a];
+            A.inv[a] = C.rp.d[a] == 0.0 ? 0.0 : __drcp_rn(C.rp.d[a]);  // = RN(1.0 / d)
         }
         A.detail_eps = P.detail_eps;
         A.coarse = P.coarse;
@@ -910,19 +912,22 @@ __device__ __noinline__ bool seg_next_leaf(const OctDev& o, SegWalk& W, const St
         const int L = (int)(node >> 57);
         const int b[3] = {(int)(node & M), (int)((node >> 19) & M), (int)((node >> 38) & M)};
         double ta, tb;
-        if (!oct_node_interval(o, L, b, A.o, A.d, A.s, ta, tb)) continue;
+        if (!oct_node_interval(o, L, b, A.o, A.d, A.inv, A.s, ta, tb)) continue;
         if (ta < W.tray0) ta = W.tray0;
         if (tb > W.tray1) tb = W.tray1;
         if (tb < ta) continue;
         const long long box = __ldg(o.box_off + L) +
                               ((long long)b[2] * __ldg(o.dims + 3 * L + 1) + b[1]) * __ldg(o.dims + 3 * L + 0) + b[0];
+        // a box whose padded range misses the window holds no leaf that
+        // does (a child's padded box lies inside its parent's): the whole
+        // subtree would emit nothing, so it is pruned without changing the
+        // emitted sequence
+        const bool meets = __ldg(o.srange + 2 * box) <= t_high && __ldg(o.srange + 2 * box + 1) >= t_low;
+        if (!meets) continue;
         if (__ldg(o.state + box) == 2) {  // leaf
-            if (__ldg(o.srange + 2 * box) <= t_high && __ldg(o.srange + 2 * box + 1) >= t_low) {
-                a0 = ta;
-                b0 = tb;
-                return true;
-            }
-            continue;
+            a0 = ta;
+            b0 = tb;
+            return true;
         }
         // children: the next level's boxes inside this one, z-major like the
         // reference's construction order (octree.py:97-105)
@@ -945,7 +950,7 @@ __device__ __noinline__ bool seg_next_leaf(const OctDev& o, SegWalk& W, const St
                 for (int cx = 0; cx < cn[0]; cx++) {
                     const int cb[3] = {c0[0] + cx, c0[1] + cy, c0[2] + cz};
                     double ca, cbb;
-                    if (!oct_node_interval(o, L + 1, cb, A.o, A.d, A.s, ca, cbb) || cbb < W.tray0 ||
+                    if (!oct_node_interval(o, L + 1, cb, A.o, A.d, A.inv, A.s, ca, cbb) || cbb < W.tray0 ||
                         ca > W.tray1)
                         continue;
                     ct[cnt] = ca;
@@ -983,6 +988,7 @@ __device__ void seg_first_hit(const Ctx<T>& C, const vc_render_params& P, const 
         A.o[a] = C.rp.o[a];
         A.d[a] = C.rp.d[a];
         A.s[a] = C.rp.s[a];
+        A.inv[a] = C.rp.d[a] == 0.0 ? 0.0 : __drcp_rn(C.rp.d[a]);  // = RN(1.0 / d)
     }
     A.detail_eps = P.detail_eps;
     A.coarse = P.coarse;
