@@ -496,7 +496,6 @@ __device__ __forceinline__ bool start_ray(Ctx<T>& C, const vc_render_params& P, 
 struct StrideArgs {
     int nx, ny, nz, adapt_jump;
     double o[3], d[3], s[3];
-    double inv[3];  // 1.0 / d (the reference's per-call value; computed once per ray)
     double detail_eps, coarse;
 };
 
@@ -557,7 +556,10 @@ __device__ __noinline__ double adaptive_stride(const OctDev o, const StrideArgs 
     const double smin = __ldg(o.srange + 2 * leaf), smax = __ldg(o.srange + 2 * leaf + 1);
     if (!(dsub(smax, smin) < A.detail_eps)) return 1.0;
     double tmin, tmax;
-    if (!oct_node_interval(o, L, b, A.o, A.d, A.inv, A.s, tmin, tmax)) return 1.0;
+    double inv[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) inv[a] = A.d[a] == 0.0 ? 0.0 : __drcp_rn(A.d[a]);  // = RN(1.0 / d)
+    if (!oct_node_interval(o, L, b, A.o, A.d, inv, A.s, tmin, tmax)) return 1.0;
     double step = (double)A.adapt_jump;
     const double kex = floor(ddiv(dsub(tmax, t_enter), A.coarse)) + 1.0;
     if (dsub(kex, k) < step) step = dsub(kex, k);
@@ -591,7 +593,6 @@ __device__ __forceinline__ void march_step(const Ctx<T>& C, const vc_render_para
             A.o[a] = C.rp.o[a];
             A.d[a] = C.rp.d[a];
             A.s[a] = C.rp.s[a];
-            A.inv[a] = C.rp.d[a] == 0.0 ? 0.0 : __drcp_rn(C.rp.d[a]);  // = RN(1.0 / d)
         }
         A.detail_eps = P.detail_eps;
         A.coarse = P.coarse;
@@ -896,6 +897,7 @@ struct SegWalk {
     unsigned long long stack[SEG_STACK];
     int sp;
     double tray0, tray1;
+    double inv[3];  // RN(1.0 / d): the reference's per-node-interval value, once per ray
 };
 
 __device__ __forceinline__ unsigned long long seg_node(int L, int bx, int by, int bz) {
@@ -912,7 +914,7 @@ __device__ __noinline__ bool seg_next_leaf(const OctDev& o, SegWalk& W, const St
         const int L = (int)(node >> 57);
         const int b[3] = {(int)(node & M), (int)((node >> 19) & M), (int)((node >> 38) & M)};
         double ta, tb;
-        if (!oct_node_interval(o, L, b, A.o, A.d, A.inv, A.s, ta, tb)) continue;
+        if (!oct_node_interval(o, L, b, A.o, A.d, W.inv, A.s, ta, tb)) continue;
         if (ta < W.tray0) ta = W.tray0;
         if (tb > W.tray1) tb = W.tray1;
         if (tb < ta) continue;
@@ -950,7 +952,7 @@ __device__ __noinline__ bool seg_next_leaf(const OctDev& o, SegWalk& W, const St
                 for (int cx = 0; cx < cn[0]; cx++) {
                     const int cb[3] = {c0[0] + cx, c0[1] + cy, c0[2] + cz};
                     double ca, cbb;
-                    if (!oct_node_interval(o, L + 1, cb, A.o, A.d, A.inv, A.s, ca, cbb) || cbb < W.tray0 ||
+                    if (!oct_node_interval(o, L + 1, cb, A.o, A.d, W.inv, A.s, ca, cbb) || cbb < W.tray0 ||
                         ca > W.tray1)
                         continue;
                     ct[cnt] = ca;
@@ -988,7 +990,6 @@ __device__ void seg_first_hit(const Ctx<T>& C, const vc_render_params& P, const 
         A.o[a] = C.rp.o[a];
         A.d[a] = C.rp.d[a];
         A.s[a] = C.rp.s[a];
-        A.inv[a] = C.rp.d[a] == 0.0 ? 0.0 : __drcp_rn(C.rp.d[a]);  // = RN(1.0 / d)
     }
     A.detail_eps = P.detail_eps;
     A.coarse = P.coarse;
@@ -997,6 +998,8 @@ __device__ void seg_first_hit(const Ctx<T>& C, const vc_render_params& P, const 
     W.stack[W.sp++] = seg_node(0, 0, 0, 0);
     W.tray0 = R.t_enter;
     W.tray1 = t_exit;
+#pragma unroll
+    for (int a = 0; a < 3; a++) W.inv[a] = A.d[a] == 0.0 ? 0.0 : __drcp_rn(A.d[a]);
     int nseg = 0;
     double s0, s1;
     bool pending = seg_next_leaf(o, W, A, P.t_low, P.t_high, s0, s1);
