@@ -905,19 +905,22 @@ __device__ __forceinline__ unsigned long long seg_node(int L, int bx, int by, in
            (unsigned long long)bx;
 }
 
-// next emitted leaf interval [a0, b0] of the walk (false: walk finished)
-__device__ __noinline__ bool seg_next_leaf(const OctDev& o, SegWalk& W, const StrideArgs& A, double t_low,
-                                           double t_high, double& a0, double& b0) {
+// One node of the walk: 1 = a leaf interval [a0, b0] was emitted, 0 = the
+// node was skipped or expanded, -1 = the walk is finished.
+constexpr int SEG_LEAF = 1, SEG_MORE = 0, SEG_DONE = -1;
+__device__ __noinline__ int seg_step(const OctDev& o, SegWalk& W, const StrideArgs& A, double t_low,
+                                     double t_high, double& a0, double& b0) {
     const unsigned M = (1u << 19) - 1u;
-    while (W.sp > 0) {
+    if (W.sp <= 0) return SEG_DONE;
+    {
         const unsigned long long node = W.stack[--W.sp];
         const int L = (int)(node >> 57);
         const int b[3] = {(int)(node & M), (int)((node >> 19) & M), (int)((node >> 38) & M)};
         double ta, tb;
-        if (!oct_node_interval(o, L, b, A.o, A.d, W.inv, A.s, ta, tb)) continue;
+        if (!oct_node_interval(o, L, b, A.o, A.d, W.inv, A.s, ta, tb)) return SEG_MORE;
         if (ta < W.tray0) ta = W.tray0;
         if (tb > W.tray1) tb = W.tray1;
-        if (tb < ta) continue;
+        if (tb < ta) return SEG_MORE;
         const long long box = __ldg(o.box_off + L) +
                               ((long long)b[2] * __ldg(o.dims + 3 * L + 1) + b[1]) * __ldg(o.dims + 3 * L + 0) + b[0];
         // a box whose padded range misses the window holds no leaf that
@@ -925,11 +928,11 @@ __device__ __noinline__ bool seg_next_leaf(const OctDev& o, SegWalk& W, const St
         // subtree would emit nothing, so it is pruned without changing the
         // emitted sequence
         const bool meets = __ldg(o.srange + 2 * box) <= t_high && __ldg(o.srange + 2 * box + 1) >= t_low;
-        if (!meets) continue;
+        if (!meets) return SEG_MORE;
         if (__ldg(o.state + box) == 2) {  // leaf
             a0 = ta;
             b0 = tb;
-            return true;
+            return SEG_LEAF;
         }
         // children: the next level's boxes inside this one, z-major like the
         // reference's construction order (octree.py:97-105)
@@ -973,13 +976,20 @@ __device__ __noinline__ bool seg_next_leaf(const OctDev& o, SegWalk& W, const St
         }
         for (int a = 0; a < cnt && W.sp < SEG_STACK; a++) W.stack[W.sp++] = ci[a];
     }
-    return false;
+    return SEG_MORE;
 }
 
-// first lattice sample in the window over the segments (R.found / R.t_hit)
-template <typename T, int INTERP>
-__device__ void seg_first_hit(const Ctx<T>& C, const vc_render_params& P, const OctDev& o, RayState& R,
-                              double t_exit, unsigned& nsamp) {
+// next emitted leaf interval [a0, b0] of the walk (false: walk finished)
+__device__ __forceinline__ bool seg_next_leaf(const OctDev& o, SegWalk& W, const StrideArgs& A, double t_low,
+                                              double t_high, double& a0, double& b0) {
+    for (;;) {
+        const int r = seg_step(o, W, A, t_low, t_high, a0, b0);
+        if (r != SEG_MORE) return r == SEG_LEAF;
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ StrideArgs make_stride_args(const Ctx<T>& C, const vc_render_params& P) {
     StrideArgs A;
     A.nx = C.v.nx;
     A.ny = C.v.ny;
@@ -993,107 +1003,156 @@ __device__ void seg_first_hit(const Ctx<T>& C, const vc_render_params& P, const 
     }
     A.detail_eps = P.detail_eps;
     A.coarse = P.coarse;
-    SegWalk W;
-    W.sp = 0;
-    W.stack[W.sp++] = seg_node(0, 0, 0, 0);
-    W.tray0 = R.t_enter;
-    W.tray1 = t_exit;
-#pragma unroll
-    for (int a = 0; a < 3; a++) W.inv[a] = A.d[a] == 0.0 ? 0.0 : __drcp_rn(A.d[a]);
-    int nseg = 0;
-    double s0, s1;
-    bool pending = seg_next_leaf(o, W, A, P.t_low, P.t_high, s0, s1);
-    while (pending) {
-        pending = false;
-        if (++nseg == SEG_CAP) {  // the reference's last buffer slot takes every later leaf
-            double a0, b0;
-            while (seg_next_leaf(o, W, A, P.t_low, P.t_high, a0, b0)) {
-                if (a0 <= dadd(s1, 1e-9)) {
-                    if (b0 > s1) s1 = b0;
-                } else {
-                    s1 = b0;
-                }
-            }
-        }
-        const double kk = floor(ddiv(dsub(s0, R.t_enter), P.coarse));
-        if (kk > R.k) R.k = kk;
-        for (;;) {
-            const double t = dadd(R.t_enter, dmul(R.k, P.coarse));
-            if (t > R.lim) return;  // every later segment starts at or after t
-            if (t > dadd(s1 > t_exit ? t_exit : s1, 1e-12)) {
-                double a0, b0;
-                if (nseg == SEG_CAP || !seg_next_leaf(o, W, A, P.t_low, P.t_high, a0, b0)) return;
-                if (a0 <= dadd(s1, 1e-9)) {  // merges into the current segment
-                    if (b0 > s1) s1 = b0;
-                    continue;
-                }
-                s0 = a0;
-                s1 = b0;
-                pending = true;
-                break;
-            }
-            double p[3];
-            C.rp.at(t, p);
-            nsamp++;
-            if (window_at<T, INTERP>(C, P, p)) {
-                R.found = true;
-                R.t_hit = t;
-                return;
-            }
-            R.k += P.use_adaptive ? adaptive_stride(o, A, p[0], p[1], p[2], R.k, R.t_enter) : 1.0;
-        }
-    }
+    return A;
 }
 
-// Kernel A for the segment mode: one ray per thread (the mode is off the
-// hot path), same work-item tiling, hit queue and counters as Kernel A.
+// Per-ray state of the segment walk between work units.
+struct SegRay {
+    double t_exit, s0, s1;
+    int nseg;
+    bool walking;  // pulling the next leaf (else marching the current segment)
+    bool has_seg;
+};
+
+// Start the next segment at leaf [a0, b0] (the reference's segment loop
+// head, _kernels.py:402-410), honouring the segment-buffer cap.
+template <typename T>
+__device__ __forceinline__ void seg_open(const Ctx<T>& C, const vc_render_params& P, const OctDev& o,
+                                         SegWalk& W, const StrideArgs& A, SegRay& S, RayState& R, double a0,
+                                         double b0) {
+    S.s0 = a0;
+    S.s1 = b0;
+    S.has_seg = true;
+    if (++S.nseg == SEG_CAP) {  // the reference's last buffer slot takes every later leaf
+        double c0, c1;
+        while (seg_next_leaf(o, W, A, P.t_low, P.t_high, c0, c1)) {
+            if (c0 <= dadd(S.s1, 1e-9)) {
+                if (c1 > S.s1) S.s1 = c1;
+            } else {
+                S.s1 = c1;
+            }
+        }
+    }
+    const double kk = floor(ddiv(dsub(S.s0, R.t_enter), P.coarse));
+    if (kk > R.k) R.k = kk;
+    S.walking = false;
+}
+
+// Kernel A for the segment mode, as a wavefront like Kernel A: persistent
+// CTAs, lanes refilled with new rays as theirs finish, and each trip of
+// the loop advances every live lane by one unit -- one node of its walk or
+// one lattice sample -- so rays with long walks do not hold their warp's
+// other lanes idle.  Same work-item tiling, hit queue and counters.
 template <typename T, int INTERP>
 __global__ void __launch_bounds__(128) firsthit_seg_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
                                                            RayPos rp0, PixelSink sink, int local_rows,
                                                            unsigned long long* counters, FrameWork* work,
                                                            HitEntry* __restrict__ hits, OctDev oct) {
+    const unsigned FULL = 0xffffffffu;
     const int tiles_x = (P.width + 7) >> 3;
     const unsigned total = (unsigned)tiles_x * (unsigned)((local_rows + 3) >> 2) * 32u;
-    const unsigned w = blockIdx.x * 128u + threadIdx.x;
     Ctx<T> C;
     init_ctx(C, P, vol, nullptr, rp0, nullptr, 0, 0, 0, TexArgs{});
     unsigned nsamp = 0, nhit = 0;
     RayState R;
-    R.found = false;
+    SegRay S;
+    SegWalk W;
+    StrideArgs A;
     int px = 0, lr = 0;
-    if (w < total) {
-        const unsigned tile = w >> 5, r = w & 31u;
-        px = (int)(tile % (unsigned)tiles_x) * 8 + (int)(r & 7u);
-        lr = (int)(tile / (unsigned)tiles_x) * 4 + (int)(r >> 3);
-        if (px < P.width && lr < local_rows) {
-            double t_exit = 0.0;
-            if (start_ray(C, P, px, image_row(P, lr), R, &t_exit)) {
-                nhit++;
-                seg_first_hit<T, INTERP>(C, P, oct, R, t_exit, nsamp);
-                if (!R.found) put_pixel(sink, P, lr, px, bg_pixel(P));
-            } else {
-                put_pixel(sink, P, lr, px, bg_pixel(P));
+    bool active = false, done = false;
+    for (;;) {
+        for (;;) {  // refill idle lanes
+            const bool want = !active && !done;
+            if (__ballot_sync(FULL, want) == 0) break;
+            const unsigned w = warp_ticket(&work->pixels, want);
+            if (want) {
+                if (w >= total) {
+                    done = true;
+                } else {
+                    const unsigned tile = w >> 5, r = w & 31u;
+                    px = (int)(tile % (unsigned)tiles_x) * 8 + (int)(r & 7u);
+                    lr = (int)(tile / (unsigned)tiles_x) * 4 + (int)(r >> 3);
+                    if (px < P.width && lr < local_rows) {
+                        if (start_ray(C, P, px, image_row(P, lr), R, &S.t_exit)) {
+                            nhit++;
+                            A = make_stride_args(C, P);
+                            W.sp = 0;
+                            W.stack[W.sp++] = seg_node(0, 0, 0, 0);
+                            W.tray0 = R.t_enter;
+                            W.tray1 = S.t_exit;
+#pragma unroll
+                            for (int a = 0; a < 3; a++) W.inv[a] = A.d[a] == 0.0 ? 0.0 : __drcp_rn(A.d[a]);
+                            S.nseg = 0;
+                            S.walking = true;
+                            S.has_seg = false;
+                            active = true;
+                        } else {
+                            put_pixel(sink, P, lr, px, bg_pixel(P));
+                        }
+                    }
+                }
             }
         }
-    }
-    const bool hit = R.found;
-    double t_star = 0.0;
-    if (hit) t_star = refine_hit<T, INTERP>(C, P, R, R.t_hit, nsamp);
-    const unsigned q = warp_ticket(&work->hits, hit);
-    if (hit) {
-        HitEntry e;
-        e.t_star = t_star;
-        e.lim = R.lim;
-        e.d[0] = C.rp.d[0];
-        e.d[1] = C.rp.d[1];
-        e.d[2] = C.rp.d[2];
-        e.ib[0] = C.sk.ib[0];
-        e.ib[1] = C.sk.ib[1];
-        e.ib[2] = C.sk.ib[2];
-        e.t_enter = R.t_enter;
-        e.lr = lr;
-        e.px = px;
-        hits[q] = e;
+        if (__all_sync(FULL, done)) break;
+        bool miss = false;
+        if (active) {
+            if (S.walking) {
+                double a0, b0;
+                const int st = seg_step(oct, W, A, P.t_low, P.t_high, a0, b0);  // one node per trip (measured best)
+                if (st == SEG_DONE) {
+                    miss = true;
+                } else if (st == SEG_LEAF) {
+                    if (S.has_seg && a0 <= dadd(S.s1, 1e-9)) {  // merges into the current segment
+                        if (b0 > S.s1) S.s1 = b0;
+                        S.walking = false;
+                    } else {
+                        seg_open(C, P, oct, W, A, S, R, a0, b0);
+                    }
+                }
+            } else {
+                const double t = dadd(R.t_enter, dmul(R.k, P.coarse));
+                if (t > R.lim) {  // every later segment starts at or after t
+                    miss = true;
+                } else if (t > dadd(S.s1 > S.t_exit ? S.t_exit : S.s1, 1e-12)) {
+                    if (S.nseg == SEG_CAP) miss = true;
+                    else S.walking = true;
+                } else {
+                    double p[3];
+                    C.rp.at(t, p);
+                    nsamp++;
+                    if (window_at<T, INTERP>(C, P, p)) {
+                        R.found = true;
+                        R.t_hit = t;
+                    } else {
+                        R.k += P.use_adaptive ? adaptive_stride(oct, A, p[0], p[1], p[2], R.k, R.t_enter) : 1.0;
+                    }
+                }
+            }
+        }
+        const bool hit = active && R.found;
+        double t_star = 0.0;
+        if (hit) t_star = refine_hit<T, INTERP>(C, P, R, R.t_hit, nsamp);
+        const unsigned q = warp_ticket(&work->hits, hit);
+        if (hit) {
+            HitEntry e;
+            e.t_star = t_star;
+            e.lim = R.lim;
+            e.d[0] = C.rp.d[0];
+            e.d[1] = C.rp.d[1];
+            e.d[2] = C.rp.d[2];
+            e.ib[0] = C.sk.ib[0];
+            e.ib[1] = C.sk.ib[1];
+            e.ib[2] = C.sk.ib[2];
+            e.t_enter = R.t_enter;
+            e.lr = lr;
+            e.px = px;
+            hits[q] = e;
+            active = false;
+        }
+        if (miss) {
+            put_pixel(sink, P, lr, px, bg_pixel(P));
+            active = false;
+        }
     }
     commit_counters(counters, 0, nsamp, 0, 0, nhit);
 }
@@ -1226,7 +1285,8 @@ static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
     const bool seg = INTERP != VC_TEX && L.p->use_adaptive && L.p->skip_empty;
     if (seg) {
         if constexpr (INTERP != VC_TEX)
-            firsthit_seg_kernel<T, INTERP><<<(unsigned)((tiles * 32 + 127) / 128), 128, 0, stream>>>(
+            firsthit_seg_kernel<T, INTERP><<<persistent_blocks(firsthit_seg_kernel<T, INTERP>, (tiles + 3) / 4), 128, 0,
+                                             stream>>>(
                 *L.p, vol, L.rp, sink, L.local_rows, reinterpret_cast<unsigned long long*>(L.counters), fw,
                 hits, L.oct);
     } else {
