@@ -3,7 +3,7 @@ scene generator of tests/test_gpu_random.py over many more seeds, each
 scene rendered by the device and the C oracle.  Prints one JSON summary
 (written to profiles/ by hand).
 
-usage: python tools/parity_sweep.py [--scenes N] [--adaptive N] [--first-seed S]
+usage: python tools/parity_sweep.py [--scenes N] [--adaptive N] [--first-seed S] [--big]
 """
 
 from __future__ import annotations
@@ -30,8 +30,17 @@ def main():
     ap.add_argument("--scenes", type=int, default=1000)
     ap.add_argument("--adaptive", type=int, default=300)
     ap.add_argument("--first-seed", type=int, default=100000)
+    ap.add_argument("--big", action="store_true",
+                    help="128^3 CT / 96^3 Marschner-Lobb / 48x40x56 noise volumes and 3x the image size")
     a = ap.parse_args()
     vols = _volumes()
+    if a.big:
+        from paper_1609_01317_b200 import phantoms
+
+        r = np.random.default_rng(77)
+        vols = {"ct": phantoms.ct_phantom(128).as_array(),
+                "noise": r.integers(0, 4096, size=(56, 40, 48)).astype(np.uint16),
+                "ml": phantoms.marschner_lobb(96).as_array()}
     names = ["ct", "noise", "ml"]
     res = {"scenes": 0, "brute_force_pixel_mismatch": 0, "count_mismatch": 0, "skipping_pixel_mismatch": 0,
            "gradient_volume_over_1lsb": 0, "gradient_volume_max_lsb": 0,
@@ -42,6 +51,8 @@ def main():
         seed = a.first_seed + n
         rng = np.random.default_rng(seed)
         vol, sc, st = _scene(rng, vols[names[n % 3]], names[n % 3])
+        if a.big:
+            st = replace(st, width=3 * st.width, height=3 * st.height)
         want, cnt = oracle.render(vol.as_array(), vol.spacing, spec_of((sc, st)))
         fb = vc.render_frame(vol, sc, replace(st, use_octree=False))
         res["scenes"] += 1
@@ -64,6 +75,8 @@ def main():
         seed = a.first_seed + 500000 + n
         rng = np.random.default_rng(seed)
         vol, sc, st = _scene(rng, vols[names[n % 3]], names[n % 3])
+        if a.big:
+            st = replace(st, width=3 * st.width, height=3 * st.height)
         vmax = float(vol.as_array().max())
         st = replace(st, use_adaptive=True, adaptive_factor=int(rng.integers(1, 9)),
                      detail_epsilon=None if rng.random() < 0.3 else float(rng.uniform(0.001, 0.3)) * vmax,
