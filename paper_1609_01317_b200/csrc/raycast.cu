@@ -1,4 +1,4 @@
-// raycast.cu -- Kernel 2: one thread per pixel, warp-tiled screen blocks.
+// raycast.cu -- Kernel 2: one ray per lane, warp-tiled screen blocks.
 //
 // Restates _kernels.render_tile (/root/reference/pkg/src/voxelcast/_kernels.py:582-797)
 // for one pixel per thread: ray generation (:639-648), ray/AABB interval
@@ -26,12 +26,14 @@
 //     evaluated samples -- and the image -- are those of the brute-force
 //     march (the invariant of pkg/tests/test_render.py:125-139).  Only
 //     use_adaptive with use_octree replays the reference's octree-segment
-//     walk (firsthit_seg_kernel), because there the samples that exist
-//     decide the pixel.
+//     walk (firsthit_seg_kernel, itself a wavefront over walk nodes and
+//     lattice samples), because there the samples that exist decide the
+//     pixel.
 //   * the shading gradient comes either from the reference taps or from
 //     the packed float4 volume of Kernel 1 (interior only; the 1-voxel
-//     boundary band always uses the taps); the scalar field either from the
-//     float64 software cascade or from tex3D (VC_SAMPLER_TEXTURE).
+//     boundary band always uses the taps, and so do samples whose corner
+//     gradients cancel, see grad_from_volume); the scalar field either from
+//     the float64 software cascade or from tex3D (VC_SAMPLER_TEXTURE).
 //   * per-warp sample / shade counters are reduced with __reduce_add_sync
 //     and committed with one atomic per warp.
 #include <cfloat>
