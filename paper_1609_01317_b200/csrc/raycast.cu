@@ -510,8 +510,8 @@ __device__ __forceinline__ bool oct_node_interval(const OctDev& o, int L, const 
 #pragma unroll
     for (int a = 0; a < 3; a++) {
         const int* iv = o.ivl + __ldg(o.ivl_off + 3 * L + a) + 2 * b[a];
-        const double lo = dmul((double)__ldg(iv), s3[a]);
-        const double hi = dmul((double)__ldg(iv + 1), s3[a]);
+        const double lo = dmul(u2d((uint32_t)__ldg(iv)), s3[a]);  // exact, FP64 pipe
+        const double hi = dmul(u2d((uint32_t)__ldg(iv + 1)), s3[a]);
         const double ov = ov3[a], d = d3[a];
         if (d == 0.0) {
             if (ov < lo || ov > hi) return false;
