@@ -65,6 +65,9 @@ def main():
             st = replace(st, gradient_source=grad, use_octree="noskip" not in parts)
             if "tex" in parts:  # hardware texture sampler
                 st = replace(st, sampler="texture")
+            if "adaptive" in parts:  # use_adaptive (with the octree: the segment walk)
+                st = replace(st, use_adaptive=True)
+                dv.ensure_octree(vol, st.octree_min_block, st.octree_max_depth)
             if "norefine" in parts:  # work accounting only: no bisection
                 st = replace(st, refine_iters=0)
             return render_params(vol, sc, st)
