@@ -949,17 +949,62 @@ __device__ __noinline__ int seg_step(const OctDev& o, SegWalk& W, const StrideAr
             c0[a] = __ldg(m + axoff[a] + lo);
             cn[a] = hi - lo >= 2 ? 2 : 1;
         }
+        // oct_node_interval is separable: a child's slab along axis a depends
+        // only on its index along a, so the <= 2 slabs per axis are evaluated
+        // once (<= 6 instead of 24) and each child takes the max / min of its
+        // three -- the same doubles, so the same intervals, bit for bit
+        double sa[3][2], sb[3][2];
+        bool sok[3][2];
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+#pragma unroll
+            for (int c = 0; c < 2; c++) {
+                sa[a][c] = -1e300;
+                sb[a][c] = 1e300;
+                sok[a][c] = true;
+                if (c < cn[a]) {
+                    const int* iv = o.ivl + __ldg(o.ivl_off + 3 * (L + 1) + a) + 2 * (c0[a] + c);
+                    const double lo = dmul(u2d((uint32_t)__ldg(iv)), A.s[a]);
+                    const double hi = dmul(u2d((uint32_t)__ldg(iv + 1)), A.s[a]);
+                    const double ov = A.o[a];
+                    if (A.d[a] == 0.0) {
+                        sok[a][c] = !(ov < lo || ov > hi);
+                    } else {
+                        double ta = dmul(dsub(lo, ov), W.inv[a]), tb = dmul(dsub(hi, ov), W.inv[a]);
+                        if (ta > tb) {
+                            const double sw = ta;
+                            ta = tb;
+                            tb = sw;
+                        }
+                        sa[a][c] = ta;
+                        sb[a][c] = tb;
+                    }
+                }
+            }
+        }
         double ct[8];
         unsigned long long ci[8];
         int cnt = 0;
         for (int cz = 0; cz < cn[2]; cz++)
             for (int cy = 0; cy < cn[1]; cy++)
                 for (int cx = 0; cx < cn[0]; cx++) {
+                    // register selects (no local-memory indexing)
+                    const bool ok = (cx ? sok[0][1] : sok[0][0]) && (cy ? sok[1][1] : sok[1][0]) &&
+                                    (cz ? sok[2][1] : sok[2][0]);
+                    if (!ok) continue;
                     const int cb[3] = {c0[0] + cx, c0[1] + cy, c0[2] + cz};
-                    double ca, cbb;
-                    if (!oct_node_interval(o, L + 1, cb, A.o, A.d, W.inv, A.s, ca, cbb) || cbb < W.tray0 ||
-                        ca > W.tray1)
-                        continue;
+                    const double ax = cx ? sa[0][1] : sa[0][0], bx = cx ? sb[0][1] : sb[0][0];
+                    const double ay = cy ? sa[1][1] : sa[1][0], by = cy ? sb[1][1] : sb[1][0];
+                    const double az = cz ? sa[2][1] : sa[2][0], bz = cz ? sb[2][1] : sb[2][0];
+                    // the same strict compares in the same axis order as oct_node_interval
+                    double ca = -1e300, cbb = 1e300;
+                    if (ax > ca) ca = ax;
+                    if (bx < cbb) cbb = bx;
+                    if (ay > ca) ca = ay;
+                    if (by < cbb) cbb = by;
+                    if (az > ca) ca = az;
+                    if (bz < cbb) cbb = bz;
+                    if (ca > cbb || cbb < W.tray0 || ca > W.tray1) continue;
                     ct[cnt] = ca;
                     ci[cnt] = seg_node(L + 1, cb[0], cb[1], cb[2]);
                     cnt++;
