@@ -715,7 +715,9 @@ __device__ __forceinline__ void put_pixel(const PixelSink& s, const vc_render_pa
     for (int r = 0; r < s.npeers; r++) s.peers[r][idx] = o;
 }
 
-struct HitEntry {  // first-hit queue: pixel, ray and refined parameter t_star
+// 16-byte aligned (96 B with the tail padding): the queue moves as six
+// 128-bit accesses per entry instead of eleven 64-bit ones (+0.8% C3)
+struct __align__(16) HitEntry {  // first-hit queue: pixel, ray and refined parameter t_star
     double t_star, lim;
     double d[3];      // ray direction (bit-exact, saves regenerating the ray)
     double ib[3];     // 1 / direction in voxel units (empty-space skipping)
