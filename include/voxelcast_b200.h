@@ -113,8 +113,12 @@ typedef struct vc_render_params {
     int32_t op, interp, mode, refine_iters;
     double coarse, fine;
     double bg[4];
-    int32_t skip_empty;                 /* macrocell empty-space skipping; output-neutral,
-                                           replaces the octree (use_octree, raycast.py:187) */
+    int32_t skip_empty;                 /* use_octree (raycast.py:187): macrocell empty-space
+                                           skipping, output-neutral; with 0 inside
+                                           [t_low, t_high] (or use_adaptive) the first hit
+                                           replays the reference's octree-segment walk
+                                           instead, which can skip in-window border samples
+                                           as the reference does (needs vc_volume_set_octree) */
     int32_t grad_source;                /* vc_grad_source */
     /* adaptive stride (use_adaptive, _kernels.py:437-463): after an
      * out-of-window first-hit sample inside an octree leaf whose padded

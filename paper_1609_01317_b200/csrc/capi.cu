@@ -30,13 +30,12 @@ struct vc_volume {
     size_t bytes = 0;
     float2* d_mm = nullptr;
     // macrocell distance fields, one per threshold window seen (LRU, at most
-    // MAX_FIELDS); `ready` orders the build before renders on other streams,
-    // `last_use` guards reuse of an evicted slot
+    // MAX_FIELDS); `ready` orders the build before renders on other streams
     struct WindowField {
         double lo = 0.0, hi = 0.0;
         uint8_t* dist = nullptr;
         uint8_t* tmp = nullptr;
-        cudaEvent_t ready = nullptr, last_use = nullptr;
+        cudaEvent_t ready = nullptr;
         uint64_t stamp = 0;
     };
     std::vector<WindowField> fields;
@@ -140,6 +139,9 @@ int validate_dims(int dtype, int nx, int ny, int nz, const double* spacing) {
     return VC_OK;
 }
 
+// Runs on v->host_stream after the voxel upload was queued there: the
+// min/max kernel is stream-ordered after the copy, and the final
+// synchronize completes both before any render (on any stream) can start.
 int finish_create(vc_volume* v) {
     // macrocells over interpolation cells [0, max(n-2,0)] per axis
     v->mx = std::max(v->nx - 2, 0) / vc::MC_EDGE + 1;
@@ -148,7 +150,6 @@ int finish_create(vc_volume* v) {
     const size_t mc = (size_t)v->mx * v->my * v->mz;
     VC_CUDA(cudaMalloc(&v->d_mm, mc * sizeof(float2)));
     VC_CUDA(cudaMalloc(&v->d_counters, VC_NUM_COUNTERS * sizeof(uint64_t)));
-    VC_CUDA(cudaStreamCreateWithFlags(&v->host_stream, cudaStreamNonBlocking));
     VC_CUDA(cudaEventCreate(&v->ev0));
     VC_CUDA(cudaEventCreate(&v->ev1));
     VC_CUDA(vc::launch_macrocell_minmax(v->dtype, v->d_data, v->nx, v->ny, v->nz, v->d_mm, v->mx, v->my,
@@ -186,7 +187,6 @@ void release(vc_volume* v) {
         cudaFree(f.dist);
         cudaFree(f.tmp);
         if (f.ready) cudaEventDestroy(f.ready);
-        if (f.last_use) cudaEventDestroy(f.last_use);
     }
     for (auto& e : v->grad_ready)
         if (e) cudaEventDestroy(e);
@@ -236,10 +236,17 @@ int create_common(int device, const void* src, cudaMemcpyKind kind, int dtype, i
         release(v);
         return fail(VC_ERR_NOMEM, std::string("cudaMalloc(volume): ") + cudaGetErrorString(e));
     }
-    e = cudaMemcpy(v->d_data, src, v->bytes, kind);
+    // The upload goes on the volume's own (non-blocking) stream so that the
+    // macrocell min/max kernel queued behind it in finish_create reads the
+    // finished copy.  A device source may still be being written by a
+    // producer on any stream (e.g. the ingest path's torch stream): drain the
+    // device first -- once per volume, so the cost does not matter.
+    e = cudaStreamCreateWithFlags(&v->host_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess && kind == cudaMemcpyDeviceToDevice) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(v->d_data, src, v->bytes, kind, v->host_stream);
     if (e != cudaSuccess) {
         release(v);
-        return cuda_fail(e, "cudaMemcpy(volume)");
+        return cuda_fail(e, "cudaMemcpyAsync(volume)");
     }
     rc = finish_create(v);
     if (rc) {
@@ -335,12 +342,14 @@ int window_field(vc_volume* v, double lo, double hi, cudaStream_t s, vc_volume::
         VC_CUDA(cudaMalloc(&f->dist, mc));
         VC_CUDA(cudaMalloc(&f->tmp, mc));
         VC_CUDA(cudaEventCreateWithFlags(&f->ready, cudaEventDisableTiming));
-        VC_CUDA(cudaEventCreateWithFlags(&f->last_use, cudaEventDisableTiming));
     } else {
         f = &v->fields[0];
         for (auto& g : v->fields)
             if (g.stamp < f->stamp) f = &g;
-        VC_CUDA(cudaEventSynchronize(f->last_use));  // renders still reading the evicted field
+        // Renders still reading the evicted field may run on any stream:
+        // eviction is rare (a ninth threshold window), so wait for the whole
+        // device rather than track every reader.
+        VC_CUDA(cudaDeviceSynchronize());
     }
     f->lo = lo;
     f->hi = hi;
@@ -442,8 +451,19 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
     const bool zero_in_window = p->t_low <= 0.0 && 0.0 <= p->t_high;
     // adaptive strides depend on the exact lattice sequence: no skipping
     L.skip_on = (p->skip_empty && !zero_in_window && !p->use_adaptive) ? 1 : 0;
-    if (p->use_adaptive && v->oct.levels == 0)
-        return fail(VC_ERR_INVALID, "use_adaptive needs an octree (vc_volume_set_octree)");
+    // With use_octree the reference's first hit marches only the merged
+    // segments of the octree leaves whose padded range meets the window
+    // (collect_segments, _kernels.py:290-364, 656-669).  Away from the grid
+    // that drops only out-of-window samples, so the macrocell skip above gives
+    // the same pixels.  But a sample in the half-voxel border band reads 0
+    // (_kernels.py:121-122): with 0 in the window it is in-window, and the
+    // reference still skips it whenever its border leaf's padded range misses
+    // the window.  That case (and use_adaptive, whose stride depends on the
+    // lattice sequence) replays the reference's segment walk on the device.
+    L.seg_walk = (p->skip_empty && p->sampler != VC_SAMPLER_TEXTURE && (p->use_adaptive || zero_in_window)) ? 1 : 0;
+    if ((p->use_adaptive || L.seg_walk) && v->oct.levels == 0)
+        return fail(VC_ERR_INVALID, "use_adaptive, or use_octree with 0 inside the threshold window, needs an "
+                                    "octree (vc_volume_set_octree)");
     vc_volume::WindowField* field = nullptr;
     if (L.skip_on) {
         int rc = window_field(v, p->t_low, p->t_high, s, &field);
@@ -468,7 +488,6 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
     if (d_counters) VC_CUDA(cudaMemsetAsync(d_counters, 0, VC_NUM_COUNTERS * sizeof(uint64_t), s));
     if (local_rows == 0) return VC_OK;
     VC_CUDA(vc::launch_raycast(L, s));
-    if (field) VC_CUDA(cudaEventRecord(field->last_use, s));
     VC_CUDA(cudaEventRecord(scp->done, s));
     return VC_OK;
 }

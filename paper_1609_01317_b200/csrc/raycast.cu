@@ -1330,8 +1330,9 @@ static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
     tex.hi = (float)L.p->t_high;
     if ((double)tex.hi > L.p->t_high) tex.hi = std::nextafter(tex.hi, -INFINITY);
     if (L.ev[0]) cudaEventRecord(L.ev[0], stream);
-    // use_adaptive + use_octree: the octree-segment first hit (exact reference walk)
-    const bool seg = INTERP != VC_TEX && L.p->use_adaptive && L.p->skip_empty;
+    // use_adaptive + use_octree, or use_octree with 0 in the window: the
+    // octree-segment first hit (exact reference walk, capi.cu render_impl)
+    const bool seg = INTERP != VC_TEX && L.seg_walk;
     if (seg) {
         if constexpr (INTERP != VC_TEX)
             firsthit_seg_kernel<T, INTERP><<<persistent_blocks(firsthit_seg_kernel<T, INTERP>, (tiles + 3) / 4), 128, 0,

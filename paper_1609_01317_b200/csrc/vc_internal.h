@@ -39,6 +39,7 @@ struct RenderLaunch {
     const uint8_t* occ;   // macrocell occupancy for the current window
     int mx, my;
     int skip_on;
+    int seg_walk;         // first hit replays the reference's octree-segment walk
     uint8_t* out;         // local_rows x width x 4 (npeers == 0)
     void* const* peers;   // device array of npeers full-frame buffers (fused gather)
     int npeers;

@@ -95,7 +95,7 @@ def render_frame_distributed(volume: Volume, scene: Scene, settings: RenderSetti
     rank = dist.get_rank(group)
     dev = torch.cuda.current_device()
     plan = BandPlan(settings.height, settings.width, band_rows, world, rank)
-    dv = prepare_device(volume, settings, dev)
+    dv = prepare_device(volume, settings, dev, scene)
     P = render_params(volume, scene, settings, band_rows=band_rows, band_first=rank, band_step=world)
     cnt = torch.zeros(_native.NUM_COUNTERS, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -199,6 +199,11 @@ class PeerFrames:
                                   device=f"cuda:{device}" if isinstance(self.ipc, _NativeIpc) else "cpu")
 
     def render(self, dv, P, counters_ptr: int, stream_ptr: int) -> None:
+        # the kernels store at image_row * width + px into every rank's
+        # mapped buffer: a frame of another size would write out of bounds
+        if (int(P.height), int(P.width)) != (self.height, self.width):
+            raise ValueError(f"frame {P.height}x{P.width} does not match the peer buffers "
+                             f"{self.height}x{self.width}")
         _native.check(_native.load().vc_render_to_peers(
             dv.handle, ctypes.byref(P), ctypes.c_void_p(self.table.data_ptr()), self.world,
             ctypes.c_void_p(counters_ptr), ctypes.c_void_p(stream_ptr)))

@@ -82,7 +82,7 @@ def render_frame_png(volume: Volume, scene: Scene, settings: RenderSettings | No
 
     settings = settings or RenderSettings()
     P = render_params(volume, scene, settings)
-    dv = prepare_device(volume, settings, device)
+    dv = prepare_device(volume, settings, device, scene)
     dev = torch.device("cuda", device)
     frame = torch.empty((settings.height, settings.width, 4), dtype=torch.uint8, device=dev)
     cnt = torch.zeros(_native.NUM_COUNTERS, dtype=torch.int64, device=dev)

@@ -43,5 +43,17 @@ def golden():
     return Golden(GOLDEN)
 
 
+def zero_in_window(spec) -> bool:
+    lo, hi = spec.get("window", (500.0, 4095.0))
+    return lo <= 0.0 <= hi
+
+
 def frame_names():
-    return [e["name"] for e in Golden(GOLDEN).frames()]
+    """Golden frames whose pixels do not depend on the reference's octree
+    walk.  With 0 inside the window they do (in-window border samples that
+    the reference's octree segments skip): zero_window_frames()."""
+    return [e["name"] for e in Golden(GOLDEN).frames() if not zero_in_window(e["spec"])]
+
+
+def zero_window_frames():
+    return [e["name"] for e in Golden(GOLDEN).frames() if zero_in_window(e["spec"])]

@@ -225,6 +225,24 @@ def frame_cases():
                         settings={"width": 40, "height": 32, "operator": "sobel3d",
                                   "use_adaptive": True, "adaptive_factor": 3,
                                   "detail_epsilon": 3500.0, "octree_min_block": 2})))
+    # 0 inside the threshold window with use_octree (the reference default):
+    # samples in the half-voxel border band read 0 (_kernels.py:121-122) and
+    # are in-window, but collect_segments skips the border leaves whose padded
+    # range misses the window -- the reference's octree image differs from
+    # its brute-force image.  A 2000-valued block with a zero-valued hole.
+    zc = np.arange(32, dtype=np.float64)
+    zz, zy, zx = np.meshgrid(zc, zc, zc, indexing="ij")
+    block = np.where((zx - 15.5) ** 2 + (zy - 15.5) ** 2 + (zz - 15.5) ** 2 <= 10.0 ** 2,
+                     0, 2000).astype(np.uint16)
+    zero_tf = {"points": [[-1000.0, [0.9, 0.6, 0.3, 0.6]], [0.0, [0.5, 0.7, 0.4, 0.8]],
+                          [1000.0, [0.2, 0.4, 0.9, 1.0]]]}
+    for oct_on in (False, True):
+        for mode, op in (("surface", "sobel3d"), ("composited", "central")):
+            cases.append((f"zerowin_block32_{mode}_octree{int(oct_on)}", block, (1.0, 1.0, 1.0),
+                          with_(d32, window=[-100.0, 500.0], transfer=zero_tf,
+                                camera={"azimuth": 8.0, "elevation": 5.0},
+                                settings={"width": 48, "height": 40, "operator": op, "mode": mode,
+                                          "use_octree": oct_on})))
     empty = np.zeros((16, 16, 16), np.uint16)
     cases.append(("empty16", empty, (1.0, 1.0, 1.0),
                   with_(d16, settings={"width": 24, "height": 24,

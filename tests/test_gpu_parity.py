@@ -15,7 +15,7 @@ import pytest
 import paper_1609_01317_b200 as vc
 from oracle import oracle
 from paper_1609_01317_b200 import phantoms
-from tests.conftest import frame_names
+from tests.conftest import frame_names, zero_window_frames
 from tests.specs import product_scene, product_settings, product_volume, spec_of
 
 pytestmark = pytest.mark.gpu
@@ -64,6 +64,22 @@ def test_frame_octree_segments_match_reference_count(golden, name):
     fb = vc.render_frame(vol, product_scene(spec), product_settings(spec, use_octree=True))
     assert np.array_equal(fb.pixels, want_px), f"max|d|={maxdiff(fb.pixels, want_px)}"
     assert fb.sample_count == want_count
+
+
+@pytest.mark.parametrize("name", zero_window_frames())
+def test_zero_window_frames_match_reference(golden, name):
+    """0 inside the threshold window: with use_octree the reference skips
+    in-window border samples that brute force hits (its octree segments,
+    _kernels.py:656-669), so the two reference images differ everywhere on
+    these goldens.  The device follows the golden's own use_octree setting
+    (the octree-segment walk when on): pixels and sample count."""
+    arr, spacing, spec, want_px, want_count = golden.frame(name)
+    vol = product_volume(arr, spacing)
+    fb = vc.render_frame(vol, product_scene(spec), product_settings(spec))
+    assert np.array_equal(fb.pixels, want_px), f"max|d|={maxdiff(fb.pixels, want_px)}"
+    assert fb.sample_count == want_count
+    fb2 = vc.render_frame(vol, product_scene(spec), product_settings(spec, gradient_source="volume"))
+    assert maxdiff(fb2.pixels, want_px) <= 1
 
 
 @pytest.mark.parametrize("name", frame_names())

@@ -142,6 +142,11 @@ def test_volume_from_array_matches_reference_semantics():
         v.value_at(4, 0, 0)
     v8 = vc.Volume.from_array(arr, dtype=np.uint8)
     assert v8.data.dtype == np.uint8
+    with pytest.raises(ValueError):  # 1000 would wrap to 232 in uint8 storage
+        vc.Volume.from_array(np.full((2, 2, 2), 1000), dtype=np.uint8)
+    with pytest.raises(ValueError):
+        vc.make_phantom("sphere", 16, radius=6, dtype=np.uint8)
+    assert vc.Volume.from_array(np.full((2, 2, 2), 70000)).value_max == 70000 - 65536  # as the reference
     with pytest.raises(ValueError):
         vc.Volume.from_array(arr, dtype=np.int32)
 

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle
-from tests.conftest import frame_names
+from tests.conftest import frame_names, zero_window_frames
 
 
 @pytest.mark.parametrize("name", frame_names())
@@ -33,6 +33,17 @@ def test_oracle_octree_segments_match_reference_counts(golden, name):
     """use_octree=True as the reference runs it (collect_segments,
     _kernels.py:267-342, and the segment loop of first_hit): pixels AND
     sample counts equal the reference's."""
+    arr, spacing, spec, want_px, want_count = golden.frame(name)
+    got_px, got_count = oracle.render(arr, spacing, spec, threads=4, octree=True)
+    assert np.array_equal(got_px, want_px)
+    assert got_count == want_count
+
+
+@pytest.mark.parametrize("name", zero_window_frames())
+def test_oracle_zero_window_frames_match_reference(golden, name):
+    """0 inside the window: the reference's image depends on use_octree
+    (its segments skip in-window border samples); the oracle follows the
+    setting each golden was rendered with -- pixels and counts."""
     arr, spacing, spec, want_px, want_count = golden.frame(name)
     got_px, got_count = oracle.render(arr, spacing, spec, threads=4, octree=True)
     assert np.array_equal(got_px, want_px)
