@@ -38,7 +38,7 @@ extern "C" {
 #define VC_API
 #endif
 
-#define VC_ABI_VERSION 2
+#define VC_ABI_VERSION 3
 #define VC_MAX_LUT 64
 
 typedef enum {
@@ -128,7 +128,10 @@ typedef struct vc_render_params {
     int32_t use_adaptive, adapt_jump;
     double detail_eps;
     int32_t sampler;                    /* vc_sampler (ABI 2) */
-    int32_t reserved0;
+    int32_t row_end;                    /* ABI 3: image rows >= row_end are not rendered
+                                           (0 = none).  render_tile's [y0, y1) band
+                                           (_kernels.py:582-627) is band_rows = 1,
+                                           band_first = y0, band_step = 1, row_end = y1 */
 } vc_render_params;
 
 /* Min/max octree in level-grid form (see paper_1609_01317_b200/octree.py):

@@ -69,7 +69,7 @@ class RenderParams(ctypes.Structure):
         ("skip_empty", ctypes.c_int32), ("grad_source", ctypes.c_int32),
         ("use_adaptive", ctypes.c_int32), ("adapt_jump", ctypes.c_int32),
         ("detail_eps", ctypes.c_double),
-        ("sampler", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+        ("sampler", ctypes.c_int32), ("row_end", ctypes.c_int32),
     ]
 
 

@@ -383,10 +383,14 @@ int validate_params(const vc_render_params* p, int* local_rows) {
         return fail(VC_ERR_INVALID, "the texture sampler is trilinear only");
     if (p->sampler == VC_SAMPLER_TEXTURE && p->use_adaptive)
         return fail(VC_ERR_UNSUPPORTED, "adaptive stepping runs on the software sampler only");
-    const long long nb = (p->height + p->band_rows - 1) / p->band_rows;
+    if (p->row_end < 0) return fail(VC_ERR_INVALID, "row_end must be >= 0");
+    // bands ascend, so the first local_rows rows of the band set are exactly
+    // those below row_end: the kernels need no extra test
+    const long long h = p->row_end > 0 ? std::min(p->height, p->row_end) : p->height;
+    const long long nb = (h + p->band_rows - 1) / p->band_rows;
     long long rows = 0;
     for (long long b = p->band_first; b < nb; b += p->band_step)
-        rows += std::min<long long>(p->band_rows, p->height - b * p->band_rows);
+        rows += std::min<long long>(p->band_rows, h - b * p->band_rows);
     if (rows > (1LL << 30)) return fail(VC_ERR_INVALID, "too many rows");
     *local_rows = (int)rows;
     return VC_OK;

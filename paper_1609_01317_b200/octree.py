@@ -156,6 +156,7 @@ class Octree:
                 assert not split.any()
         self.node_count = int(sum(e.sum() for e in self.exists))
         self._root = None
+        self._flat = None
 
     # ------------------------------------------------------------ reference API
 
@@ -196,35 +197,121 @@ class Octree:
 
     def device_arrays(self):
         """Flat arrays of vc_octree_desc (include/voxelcast_b200.h)."""
-        nx, ny, nz = self.volume_dims
-        levels = self.depth + 1
-        dims = np.zeros((levels, 3), np.int32)
-        amap = np.zeros((levels, nx + ny + nz), np.int32)
-        ivl_off = np.zeros((levels, 3), np.int32)
-        box_off = np.zeros(levels, np.int64)
-        ivl, state, srange = [], [], []
-        off = 0
-        boff = 0
-        for L in range(levels):
-            for a, n in enumerate((nx, ny, nz)):
-                iv = self.ax[a][0][L]
-                dims[L, a] = len(iv)
-                ivl_off[L, a] = off
-                ivl.append(iv.astype(np.int32).ravel())
-                off += 2 * len(iv)
-                base = (0, nx, nx + ny)[a]
-                amap[L, base:base + n] = np.repeat(np.arange(len(iv), dtype=np.int32), iv[:, 1] - iv[:, 0])
-            st = np.where(self.leaf[L], 2, np.where(self.exists[L], 1, 0)).astype(np.uint8)
-            box_off[L] = boff
-            boff += st.size
-            state.append(st.ravel())
-            r = self.ranges[L]
-            srange.append(np.stack([r["smin"], r["smax"]], axis=-1).astype(np.float64).ravel())
-        return {
-            "levels": levels, "dims": dims.ravel(), "axis_map": amap.ravel(),
-            "ivl_off": ivl_off.ravel(), "ivl": np.concatenate(ivl), "box_off": box_off,
-            "state": np.concatenate(state), "srange": np.concatenate(srange),
-        }
+        states = [np.where(self.leaf[L], 2, np.where(self.exists[L], 1, 0)).astype(np.uint8)
+                  for L in range(self.depth + 1)]
+        sranges = [np.stack([r["smin"], r["smax"]], axis=-1).astype(np.float64) for r in self.ranges]
+        return _pack_levels(self.volume_dims, self.ax, states, sranges)
+
+
+def _pack_levels(volume_dims, ax, states, sranges):
+    """vc_octree_desc arrays from per-level axis intervals, box states
+    (0 absent, 1 internal, 2 leaf; [bz, by, bx]) and padded ranges."""
+    nx, ny, nz = volume_dims
+    levels = len(states)
+    dims = np.zeros((levels, 3), np.int32)
+    amap = np.zeros((levels, nx + ny + nz), np.int32)
+    ivl_off = np.zeros((levels, 3), np.int32)
+    box_off = np.zeros(levels, np.int64)
+    ivl, state, srange = [], [], []
+    off = 0
+    boff = 0
+    for L in range(levels):
+        for a, n in enumerate((nx, ny, nz)):
+            iv = ax[a][0][L]
+            dims[L, a] = len(iv)
+            ivl_off[L, a] = off
+            ivl.append(iv.astype(np.int32).ravel())
+            off += 2 * len(iv)
+            base = (0, nx, nx + ny)[a]
+            amap[L, base:base + n] = np.repeat(np.arange(len(iv), dtype=np.int32), iv[:, 1] - iv[:, 0])
+        box_off[L] = boff
+        boff += states[L].size
+        state.append(states[L].ravel())
+        srange.append(np.asarray(sranges[L], np.float64).ravel())
+    return {
+        "levels": levels, "dims": dims.ravel(), "axis_map": amap.ravel(),
+        "ivl_off": ivl_off.ravel(), "ivl": np.concatenate(ivl), "box_off": box_off,
+        "state": np.concatenate(state), "srange": np.concatenate(srange),
+    }
+
+
+def flat_arrays(tree: Octree):
+    """The reference's array form of the tree (octree.py:114-135): per node
+    voxel bounds (lo, hi), exact and padded ranges, child indices (-1
+    padded), nodes in the reference's depth-first order.  Cached on the tree."""
+    cached = getattr(tree, "_flat", None)
+    if cached is not None:
+        return cached
+    nodes: list[OctreeNode] = []
+    stack = [tree.root]
+    while stack:
+        n = stack.pop()
+        nodes.append(n)
+        stack.extend(n.children)
+    index = {id(n): i for i, n in enumerate(nodes)}
+    cnt = len(nodes)
+    nbounds = np.empty((cnt, 6), np.int32)
+    vminmax = np.empty((cnt, 2), np.float64)
+    sminmax = np.empty((cnt, 2), np.float64)
+    nchildren = np.full((cnt, 8), -1, np.int32)
+    for i, n in enumerate(nodes):
+        nbounds[i] = (*n.lo, *n.hi)
+        vminmax[i] = (n.vmin, n.vmax)
+        sminmax[i] = (n.smin, n.smax)
+        for c, ch in enumerate(n.children):
+            nchildren[i, c] = index[id(ch)]
+    tree._flat = (nbounds, vminmax, sminmax, nchildren)
+    return tree._flat
+
+
+def device_arrays_from_flat(volume_dims, nbounds, sminmax, nchildren):
+    """vc_octree_desc arrays of a tree given in the reference's flat form
+    (what _kernels.render_tile receives, _kernels.py:582-627).  Every split
+    halves an axis interval the same way wherever it sits (octree.py:93-107),
+    so the nodes of depth L lie on the level-L interval grid; this places
+    each node there.  Raises ValueError for arrays that are not such a tree."""
+    nb = np.asarray(nbounds, np.int64).reshape(-1, 6)
+    sm = np.asarray(sminmax, np.float64).reshape(-1, 2)
+    ch = np.asarray(nchildren, np.int64).reshape(-1, 8)
+    n = len(nb)
+    if n == 0 or len(sm) < n or len(ch) < n:
+        raise ValueError("octree arrays are empty or of unequal length")
+    depth = np.full(n, -1, np.int64)
+    depth[0] = 0
+    order = [0]
+    for i in order:  # breadth first from the root
+        for c in ch[i]:
+            if c < 0:
+                break
+            if not 0 < c < n or depth[c] >= 0:
+                raise ValueError("octree child index out of range or repeated")
+            depth[c] = depth[i] + 1
+            order.append(int(c))
+    if len(order) != n:
+        raise ValueError("octree has unreachable nodes")
+    D = int(depth.max())
+    if D > 16:
+        raise ValueError("octree deeper than 16 levels")
+    ax = [_axis_levels(d, D) for d in volume_dims]
+    states, sranges = [], []
+    for L in range(D + 1):
+        sel = np.nonzero(depth == L)[0]
+        idx = []
+        for a in range(3):
+            iv = ax[a][0][L]
+            k = np.searchsorted(iv[:, 0], nb[sel, a])
+            k = np.minimum(k, len(iv) - 1)
+            if not (np.array_equal(iv[k, 0], nb[sel, a]) and np.array_equal(iv[k, 1], nb[sel, 3 + a])):
+                raise ValueError(f"octree node bounds at depth {L} are not the reference's halving split")
+            idx.append(k)
+        shape = (len(ax[2][0][L]), len(ax[1][0][L]), len(ax[0][0][L]))
+        st = np.zeros(shape, np.uint8)
+        sr = np.zeros(shape + (2,), np.float64)
+        st[idx[2], idx[1], idx[0]] = np.where(ch[sel, 0] < 0, 2, 1)
+        sr[idx[2], idx[1], idx[0]] = sm[sel]
+        states.append(st)
+        sranges.append(sr)
+    return _pack_levels(tuple(int(d) for d in volume_dims), ax, states, sranges)
 
 
 def build_octree(volume: Volume, min_block: int = 4, max_depth: int = 8) -> Octree:

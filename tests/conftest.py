@@ -13,12 +13,48 @@ import pytest
 ROOT = Path(__file__).resolve().parents[1]
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
+# `import voxelcast` -> pkg/src/voxelcast, the drop-in at the reference's
+# module name (what tests/reference_suite imports)
+PKG_SRC = ROOT / "pkg" / "src"
+if str(PKG_SRC) not in sys.path:
+    sys.path.insert(0, str(PKG_SRC))
 
 GOLDEN = Path(__file__).resolve().parent / "golden" / "golden.npz"
+REFERENCE_SUITE = Path(__file__).resolve().parent / "reference_suite"
+
+# The reference's hot-path test modules run unmodified against the drop-in
+# (tests/reference_suite/README.md).  Every case renders, samples or takes
+# gradients on the device, so the whole directory is -m gpu.  Outcomes that
+# differ from "pass", each with its reason:
+REFERENCE_SUITE_XFAIL = {
+    # red by design in the reference too (pkg/README.md:34-39,
+    # pkg/test_output.txt:220-221): 12.9 deg mean central-difference error on
+    # a hard binary shell; the device gradients are bit-identical to the
+    # reference's, so the same assertion fails the same way
+    "test_acceptance.py::test_gradient_operators_are_correct":
+        "reference red-by-design check (CD < 5 deg on a binary shell), fails identically in the reference",
+}
+REFERENCE_SUITE_SKIP = {
+    "test_acceptance.py::test_service_round_trip_applies_and_rejects_controls":
+        "the FastAPI websocket service is out of scope (SURVEY.md §2)",
+}
 
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the sm_100a library")
+
+
+def pytest_collection_modifyitems(config, items):
+    for item in items:
+        path = Path(str(item.fspath))
+        if REFERENCE_SUITE not in path.parents:
+            continue
+        item.add_marker(pytest.mark.gpu)
+        key = f"{path.name}::{getattr(item, 'originalname', item.name)}"
+        if key in REFERENCE_SUITE_XFAIL:
+            item.add_marker(pytest.mark.xfail(reason=REFERENCE_SUITE_XFAIL[key], strict=True))
+        if key in REFERENCE_SUITE_SKIP:
+            item.add_marker(pytest.mark.skip(reason=REFERENCE_SUITE_SKIP[key]))
 
 
 class Golden:
