@@ -39,6 +39,12 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "frames/sec and Gsamples/s, 512³ volume @1920×1080, at 1/2/4/8 B200 vs CPU ref"
 UNIT = "frames/s"
+# what the timed configuration computes in (gradient_source="volume"): the
+# value, opacity, window tests and compositing in float64 as the reference;
+# the shading gradient is interpolated from Kernel 1's float32 volume and the
+# diffuse term formed in float32 (<= 1/255); exact_fp64_path is
+# the all-float64 configuration
+DTYPE_LABEL = "f64 value/opacity/composite; f32 gradient volume + diffuse"
 
 
 def parse():
@@ -63,6 +69,10 @@ def parse():
                     help="warm-up + timed frames only (for the ncu launch-list pass); reduced JSON line")
     ap.add_argument("--gather", default="peer", choices=("peer", "nccl"),
                     help="N>1: fused NVLink peer stores (validated) or NCCL all-gather")
+    ap.add_argument("--no-side-configs", action="store_true",
+                    help="skip the C1 / C2 / C4 / C5 side measurements")
+    ap.add_argument("--no-numba", action="store_true",
+                    help="skip timing the unmodified numba reference (baseline/_ref)")
     return ap.parse_args()
 
 
@@ -225,6 +235,252 @@ def workload_config(args) -> dict:
             "mode": args.mode}
 
 
+class _GridStub:
+    """The few Volume attributes render_params / default_scene read, for a
+    grid that only exists on the device (C4: 4 GiB, never copied to host)."""
+
+    def __init__(self, dims, vmin, vmax, dtype):
+        self.dims = tuple(dims)
+        self.spacing = (1.0, 1.0, 1.0)
+        self.extent = tuple(float(n) for n in dims)
+        self.value_min, self.value_max = vmin, vmax
+        self.data = np.empty(0, dtype)
+
+
+def _timed_frames(L, dv, vol, frame, stream, flush, first, n, out_ptr, counters_ptr=None):
+    """Device time of n frames (CUDA events on the launching stream, L2
+    flushed between frames outside the event pair); returns per-frame ms."""
+    import ctypes
+
+    import torch
+
+    from paper_1609_01317_b200 import _native
+    from paper_1609_01317_b200.raycast import render_params
+
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    ms = []
+    for k in range(n):
+        sc, st = frame(first + k)
+        P = render_params(vol, sc, st)
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _native.check(L.vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(out_ptr),
+                                  ctypes.c_void_p(counters_ptr) if counters_ptr else None, sp))
+        e1.record(stream)
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    return ms
+
+
+def side_config(name, desc, vol, dv, scene_fn, frames, dev, L, stream, flush, peak):
+    """fps / Gsamples/s / parity of one BASELINE render config on one GPU,
+    timed like the headline (device time, inputs resident, L2 flushed)."""
+    import ctypes
+    from dataclasses import replace
+
+    import torch
+
+    from paper_1609_01317_b200 import _native
+    from paper_1609_01317_b200.raycast import render_params
+
+    sc0, st0 = scene_fn(0)
+    H, W = st0.height, st0.width
+    out = torch.empty((H, W, 4), dtype=torch.uint8, device=f"cuda:{dev}")
+    ref = torch.empty_like(out)
+    cnt = torch.zeros(_native.NUM_COUNTERS, dtype=torch.int64, device=f"cuda:{dev}")
+    res = {"workload": desc}
+    variants = {"volume": dict(gradient_source="volume"), "taps": dict(gradient_source="taps"),
+                "texture": dict(gradient_source="volume", sampler="texture")}
+    bf = np.zeros(_native.NUM_COUNTERS)
+    nbf = 2
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    for k in range(nbf):  # brute-force work counts (the reference's W and K), untimed
+        sc, st = scene_fn(10 + k)
+        P = render_params(vol, sc, replace(st, use_octree=False, gradient_source="taps"))
+        _native.check(L.vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(ref.data_ptr()),
+                                  ctypes.c_void_p(cnt.data_ptr()), sp))
+        torch.cuda.synchronize(dev)
+        bf += cnt.cpu().numpy()
+    bf /= nbf
+    w_frame, k_frame = bf[0] + bf[1], bf[1]
+    res["W_ray_samples_bruteforce"] = float(w_frame)
+    res["K_shades_bruteforce"] = float(k_frame)
+    for vname, kw in variants.items():
+        fr = lambda i, kw=kw: (lambda s: (s[0], replace(s[1], **kw)))(scene_fn(i))
+        _timed_frames(L, dv, vol, fr, stream, flush, 0, 3, out.data_ptr())  # warm-up (+ lazy builds)
+        with ClockSampler(dev) as clk:
+            ms = _timed_frames(L, dv, vol, fr, stream, flush, 10, frames, out.data_ptr())
+        fps = 1000.0 / float(np.mean(ms))
+        # executed work of this variant, one frame
+        sc, st = fr(10)
+        P = render_params(vol, sc, st)
+        _native.check(L.vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(out.data_ptr()),
+                                  ctypes.c_void_p(cnt.data_ptr()), sp))
+        sc, st = scene_fn(10)
+        P = render_params(vol, sc, replace(st, use_octree=False, gradient_source="taps"))
+        _native.check(L.vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(ref.data_ptr()), None, sp))
+        torch.cuda.synchronize(dev)
+        ce = cnt.cpu().numpy()
+        d = (out.to(torch.int16) - ref.to(torch.int16)).abs().amax(dim=2)
+        res[vname] = {
+            "fps": fps, "ms_per_frame": float(np.mean(ms)), "frames": frames,
+            "gsamples_per_s_bruteforce": w_frame * fps / 1e9,
+            "gsamples_per_s_executed": float(ce[0] + ce[1]) * fps / 1e9,
+            "logical_GBps": (8 * vol.data.dtype.itemsize * w_frame + 128 * k_frame + 4 * H * W) * fps / 1e9,
+            "vs_fp64_taps_bruteforce": {"max_abs_diff": int(d.max().item()),
+                                        "pixels_differing": int((d > 0).sum().item()),
+                                        "frac_within_1": float((d <= 1).float().mean().item())},
+            "clocks": clk.summary()}
+    res["logical_GBps_note"] = (f"8*bpv per brute-force ray sample + 128 per shade + 4 per pixel, "
+                                f"vs measured HBM {peak:.1f} GB/s (frac > 1 possible: skipping)")
+    res["parity_note"] = ("vs the device's bit-exact float64 taps brute-force path on one frame; that path "
+                          "is bit-exact vs the oracle on whole frames / row bands (tests/test_gpu_fullsize.py)")
+    return res
+
+
+def prepass_rate(L, dv, n, bpv, dev, stream, peak, reps=5):
+    """Kernel 1 (gradient pre-pass) GB/s for the three operators: bytes per
+    voxel = bpv in + 16 out, CUDA events, best and mean."""
+    import ctypes
+
+    import torch
+
+    from paper_1609_01317_b200 import _native
+
+    out = torch.empty((n, n, n, 4), dtype=torch.float32, device=f"cuda:{dev}")
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    res = {}
+    for op, code in (("central", 0), ("sobel3d", 1), ("zucker-hummel", 2)):
+        _native.check(L.vc_gradient_prepass_into(dv.handle, code, ctypes.c_void_p(out.data_ptr()), sp))
+        with ClockSampler(dev) as clk:
+            ms = []
+            for _ in range(reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                _native.check(L.vc_gradient_prepass_into(dv.handle, code, ctypes.c_void_p(out.data_ptr()), sp))
+                e1.record(stream)
+                e1.synchronize()
+                ms.append(e0.elapsed_time(e1))
+        gbs = n ** 3 * (bpv + 16) / (float(np.mean(ms)) / 1000.0) / 1e9
+        res[op] = {"ms": float(np.mean(ms)), "GBps": gbs, "frac": gbs / peak,
+                   "best_GBps": n ** 3 * (bpv + 16) / (min(ms) / 1000.0) / 1e9, "clocks": clk.summary()}
+    del out
+    return res
+
+
+def side_configs(args, dev, L, stream, flush, ct_vol, ct_dv):
+    """BASELINE.json configs other than the headline, each on one GPU with
+    its own clocks: C1, C2, C4 render rates and C5 pre-pass rates."""
+    import torch
+
+    import paper_1609_01317_b200 as vc
+    from paper_1609_01317_b200 import phantoms
+    from paper_1609_01317_b200.volume import DeviceVolume
+
+    peak, _ = peaks()
+    out = {}
+    t0 = time.perf_counter()
+    c1 = phantoms.sphere_c1(64)
+    out["C1"] = side_config("C1", "C1: 64^3 uint8 sphere, 256x256, central difference, surface, single view",
+                            c1, vc.device_volume(c1, dev), lambda i: phantoms.scene_c1(c1), 30, dev, L,
+                            stream, flush, peak)
+    c2 = phantoms.marschner_lobb(256)
+    out["C2"] = side_config("C2", "C2: 256^3 uint8 Marschner-Lobb, 1024x1024, Sobel3D, surface, "
+                                  "1 deg/frame orbit", c2, vc.device_volume(c2, dev),
+                            lambda i: phantoms.scene_c2(c2, azimuth=float(i)), 30, dev, L, stream, flush, peak)
+    # C4: the grid is made on the device and handed over device to device
+    t = phantoms.fbm_noise_tensor(1024, device=f"cuda:{dev}")
+    vmin, vmax = float(t.min().item()), float(t.max().item())
+    c4 = _GridStub((1024, 1024, 1024), vmin, vmax, np.float32)
+    c4_dv = DeviceVolume.from_device(dev, t.data_ptr(), np.float32, c4.dims, c4.spacing)
+    del t
+    torch.cuda.empty_cache()
+    c4_dv.gradient_prepass(1)
+    out["C4"] = side_config("C4", "C4: 1024^3 float32 fBm noise, 3840x2160, Sobel3D, composited, whole frame "
+                                  "on ONE GPU (the 8-GPU config's full frame)", c4, c4_dv,
+                            lambda i: phantoms.scene_c4(c4, azimuth=float(i)), 10, dev, L, stream, flush, peak)
+    # C5: Kernel 1 over the headline CT grid (512^3 u16) and the C4 grid (1024^3 f32)
+    c4_dv.close()  # frees the C4 gradient volume before the 16 GiB pre-pass output
+    torch.cuda.empty_cache()
+    out["C5"] = {"workload": "C5: gradient pre-pass, GB/s vs the measured HBM peak (bpv in + 16 B out per voxel)",
+                 "512^3 uint16 CT": prepass_rate(L, ct_dv, 512, 2, dev, stream, peak)}
+    t = phantoms.fbm_noise_tensor(1024, device=f"cuda:{dev}")
+    big = DeviceVolume.from_device(dev, t.data_ptr(), np.float32, (1024, 1024, 1024), (1.0, 1.0, 1.0))
+    del t
+    torch.cuda.empty_cache()
+    out["C5"]["1024^3 float32 fBm"] = prepass_rate(L, big, 1024, 4, dev, stream, peak, reps=3)
+    big.close()
+    torch.cuda.empty_cache()
+    out["wall_s"] = time.perf_counter() - t0
+    return out
+
+
+def reference_numba(vol, frame, args, timeout_s=600):
+    """The UNMODIFIED reference (numba render_frame, baseline/_ref) on the
+    host's cores, in a child process: >= 2 C3 frames with the octree on (tree
+    built once and passed in, the reference bench's convention, bench.py:103-106)
+    and >= 2 with it off, after a JIT warm-up.  None when not installed."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "voxelcast" / "raycast.py").exists():
+        return {"unavailable": "baseline/_ref not installed"}
+    import tempfile
+
+    tmp = Path(tempfile.mkdtemp(prefix="vc_numba_"))
+    np.save(tmp / "vol.npy", vol.as_array())
+    sc, st = frame(args.warmup)
+    spec = {"az0": float(sc.camera.azimuth), "eye": list(sc.camera.eye), "target": list(sc.camera.target),
+            "light": list(sc.light.position), "width": st.width, "height": st.height, "op": st.operator.value,
+            "mode": st.mode}
+    (tmp / "spec.json").write_text(json.dumps(spec))
+    code = r"""
+import json, os, sys, time
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import voxelcast as v
+assert 'baseline' in v.__file__, v.__file__
+from voxelcast.octree import build_octree
+tmp = sys.argv[2]
+s = json.load(open(os.path.join(tmp, 'spec.json')))
+vol = v.Volume.from_array(np.load(os.path.join(tmp, 'vol.npy')))
+def scene(i):
+    return v.Scene(camera=v.Camera(eye=tuple(s['eye']), target=tuple(s['target']), azimuth=s['az0'] + i),
+                   light=v.Light(position=tuple(s['light'])))
+st = v.RenderSettings(width=s['width'], height=s['height'], operator=v.OperatorKind(s['op']), mode=s['mode'])
+t0 = time.perf_counter(); v.render_frame(vol, scene(0), v.RenderSettings(width=32, height=18,
+    operator=st.operator, mode=st.mode)); jit = time.perf_counter() - t0
+t0 = time.perf_counter(); tree = build_octree(vol); tb = time.perf_counter() - t0
+res = {'jit_warmup_s': jit, 'octree_build_s': tb, 'workers': os.cpu_count()}
+from dataclasses import replace
+for name, stt, kw in (('octree_on', st, {'octree': tree}), ('octree_off', replace(st, use_octree=False), {})):
+    ms = []
+    for i in range(2):
+        fb = v.render_frame(vol, scene(1 + i), stt, **kw)
+        ms.append(fb.render_ms)
+    res[name] = {'render_ms': ms, 'fps': 1000.0 / float(np.median(ms)), 'sample_count': int(fb.sample_count)}
+print(json.dumps(res))
+"""
+    env = dict(os.environ, NUMBA_CACHE_DIR=str(tmp / "numba_cache"))
+    try:
+        r = subprocess.run([sys.executable, "-c", code, str(ref), str(tmp)], capture_output=True, text=True,
+                           timeout=timeout_s, env=env)
+        if r.returncode != 0:
+            return {"unavailable": f"numba reference failed: {r.stderr.strip().splitlines()[-1:]}"}
+        res = json.loads(r.stdout.strip().splitlines()[-1])
+    except subprocess.TimeoutExpired:
+        return {"unavailable": f"numba reference exceeded {timeout_s} s"}
+    finally:
+        import shutil
+
+        shutil.rmtree(tmp, ignore_errors=True)
+    best = max(res["octree_on"]["fps"], res["octree_off"]["fps"])
+    return {"value": best, "unit": UNIT, "cores": res["workers"], "kind": "reference",
+            "sample": "unmodified numba voxelcast.render_frame from baseline/_ref, workers=os.cpu_count(), "
+                      "2 C3 frames each with the octree on (built once, passed in) and off, median render_ms; "
+                      "value = the faster setting",
+            **res}
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -381,7 +637,8 @@ def run_ours(args):
             print(json.dumps({"metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world,
                               "steps": args.steps, "warmup": args.warmup,
                               "ms_per_step": ms_total / args.steps, "higher_is_better": True,
-                              "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                              "scaling": "strong", "vs_baseline": None,
+                              "dtype": DTYPE_LABEL if args.grad == "volume" else "f64",
                               "data": "synthetic", "timed_only": True,
                               "config": {**workload_config(args), "gradient_source": args.grad,
                                          "gather": gather_mode},
@@ -571,6 +828,13 @@ def run_ours(args):
                "sample": f"C oracle port of _kernels.render_tile (brute force, float64), {sample}; "
                          f"cpu: {lscpu_model()}"}
 
+    if cpu is not None and not args.no_numba:
+        cpu["reference_numba"] = reference_numba(vol, frame, args)
+
+    side = None
+    if not args.no_side_configs and world == 1:
+        side = side_configs(args, dev, L, stream, flush, vol, dv)
+
     bpv = vol.data.dtype.itemsize
     # algorithmic (logical) bytes: 8*bpv per ray sample,
     # 128 per shade (8 float4 gradient taps), 4 per output pixel
@@ -594,7 +858,8 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": DTYPE_LABEL if args.grad == "volume" else "f64", "data": "synthetic",
         "config": {**workload_config(args), "gradient_source": args.grad,
                    "empty_space_skipping": not args.no_skip,
                    "l2": "flushed between timed frames (256 MiB write, outside the event pair)",
@@ -639,6 +904,7 @@ def run_ours(args):
            if backend != "nccl" and world > 1 else {}),
         "exact_fp64_path": exact,
         "texture_path": texture,
+        "side_configs": side,
         "wall_s_timed_region": t_wall,
     }
     print(json.dumps(line), flush=True)

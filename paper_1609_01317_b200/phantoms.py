@@ -180,6 +180,15 @@ def fbm_noise(n: int = 1024, octaves: int = 5, seed: int = 1609, base_cells: int
 
 
 def _fbm_noise_torch(n, octaves, seed, base_cells, dtype, device) -> Volume:
+    out = fbm_noise_tensor(n, octaves, seed, base_cells, device).cpu().numpy()
+    return Volume.from_array(out, dtype=dtype)
+
+
+def fbm_noise_tensor(n: int = 1024, octaves: int = 5, seed: int = 1609, base_cells: int = 8,
+                     device: str = "cuda"):
+    """fbm_noise evaluated with torch on `device`, returned as the (n, n, n)
+    float32 device tensor itself (no host copy): bench.py's C4 side config
+    hands it to the library with vc_volume_create_device."""
     import torch
 
     c = (torch.arange(n, dtype=torch.float64, device=device) + 0.5) / n
@@ -201,9 +210,9 @@ def _fbm_noise_torch(n, octaves, seed, base_cells, dtype, device) -> Volume:
             wz = w[z0:z1, None, None]
             acc[z0:z1] += (0.5 ** o) * (txy[i[z0:z1]] * (1.0 - wz) + txy[i[z0:z1] + 1] * wz)
         del tx, txy
-    out = (acc / total_amp * 4095.0).to(torch.float32).cpu().numpy()
+    out = (acc / total_amp * 4095.0).to(torch.float32)
     del acc
-    return Volume.from_array(out, dtype=dtype)
+    return out
 
 
 # ------------------------------------------------------------------ scenes
