@@ -231,7 +231,9 @@ int create_common(int device, const void* src, cudaMemcpyKind kind, int dtype, i
     v->nz = nz;
     for (int a = 0; a < 3; a++) v->spacing[a] = spacing[a];
     v->bytes = (size_t)nx * ny * nz * dtype_size(dtype);
-    cudaError_t e = cudaMalloc(&v->d_data, v->bytes);
+    // zeroed tail padding: gather8 reads one element past an x-degenerate row
+    cudaError_t e = cudaMalloc(&v->d_data, v->bytes + vc::VC_VOLUME_PAD);
+    if (e == cudaSuccess) e = cudaMemset(static_cast<char*>(v->d_data) + v->bytes, 0, vc::VC_VOLUME_PAD);
     if (e != cudaSuccess) {
         release(v);
         return fail(VC_ERR_NOMEM, std::string("cudaMalloc(volume): ") + cudaGetErrorString(e));
@@ -363,6 +365,8 @@ int window_field(vc_volume* v, double lo, double hi, cudaStream_t s, vc_volume::
 int validate_params(const vc_render_params* p, int* local_rows) {
     if (p == nullptr) return fail(VC_ERR_INVALID, "params is null");
     if (p->width <= 0 || p->height <= 0) return fail(VC_ERR_INVALID, "image size must be positive");
+    if (p->width > 65535 || p->height > 65535)  // hit-queue entries pack (row, column) in 16 bits each
+        return fail(VC_ERR_UNSUPPORTED, "frames wider or taller than 65535 pixels are not supported");
     if (p->band_rows < 1 || p->band_step < 1 || p->band_first < 0)
         return fail(VC_ERR_INVALID, "band_rows/band_step must be >= 1 and band_first >= 0");
     if (p->lut_n < 1 || p->lut_n > VC_MAX_LUT) return fail(VC_ERR_INVALID, "lut_n must be in [1, VC_MAX_LUT]");

@@ -69,6 +69,19 @@ __device__ __forceinline__ double lerp(double f0, double f1, double t) {
     return dadd(f0, dmul(dsub(f1, f0), t));
 }
 
+// integer voxels are carried in 32-bit registers once loaded (zero
+// extended), float voxels as themselves
+template <typename T>
+struct Wide {
+    using type = uint32_t;
+};
+template <>
+struct Wide<float> {
+    using type = float;
+};
+template <typename T>
+using wide_t = typename Wide<T>::type;
+
 template <typename T>
 struct Vol {
     const T* __restrict__ data;
@@ -82,6 +95,7 @@ struct Vol {
     // +1 corner along x / y / z (0 on a one-voxel axis, _kernels.py:53-64)
     int kx, ky, kz;
     uint32_t sx1, sy1, sz1;
+    uint32_t syb, szb;  // sy1 / sz1 in bytes
 };
 
 template <typename T>
@@ -104,7 +118,40 @@ __host__ __device__ inline Vol<T> make_vol(const T* data, int nx, int ny, int nz
     v.sx1 = nx > 1 ? 1u : 0u;
     v.sy1 = ny > 1 ? (uint32_t)nx : 0u;
     v.sz1 = nz > 1 ? (uint32_t)nx * (uint32_t)ny : 0u;
+    v.syb = v.sy1 * (uint32_t)sizeof(T);
+    v.szb = v.sz1 * (uint32_t)sizeof(T);
     return v;
+}
+
+// The 8 corners of the (clamped) cell with lower corner (i, j, k): one
+// 64-bit base address and two row offsets, the x neighbours at an
+// immediate +1 element (x-degenerate grids, nx == 1, read the same voxel
+// twice on a uniform branch).  Corner order c000 c100 c010 c110 c001 c101
+// c011 c111.
+// The +1 reads of an x-degenerate grid land on the next row or on the
+// allocation's zeroed tail padding (VC_VOLUME_PAD) and are replaced.
+constexpr size_t VC_VOLUME_PAD = 64;
+template <typename T>
+__device__ __forceinline__ void gather8(const Vol<T>& v, int i, int j, int k, wide_t<T> c[8]) {
+    const uint32_t idx = ((uint32_t)k * (uint32_t)v.ny + (uint32_t)j) * (uint32_t)v.nx + (uint32_t)i;
+    const T* p0 = v.data + idx;
+    const T* p1 = reinterpret_cast<const T*>(reinterpret_cast<const char*>(p0) + v.syb);
+    const T* p2 = reinterpret_cast<const T*>(reinterpret_cast<const char*>(p0) + v.szb);
+    const T* p3 = reinterpret_cast<const T*>(reinterpret_cast<const char*>(p2) + v.syb);
+    c[0] = __ldg(p0);
+    c[1] = __ldg(p0 + 1);
+    c[2] = __ldg(p1);
+    c[3] = __ldg(p1 + 1);
+    c[4] = __ldg(p2);
+    c[5] = __ldg(p2 + 1);
+    c[6] = __ldg(p3);
+    c[7] = __ldg(p3 + 1);
+    if (v.sx1 == 0u) {
+        c[1] = c[0];
+        c[3] = c[2];
+        c[5] = c[4];
+        c[7] = c[6];
+    }
 }
 
 template <typename T>
@@ -199,7 +246,7 @@ struct VoxelBits<float> {
 // lerp(c0, c1, t) = c0 + (c1 - c0) * t over two voxel values, bit-identical
 // to the reference's float64 expression (c1 - c0 is exact for integer data).
 template <typename T>
-__device__ __forceinline__ double lerp_vox(T c0, T c1, double t) {
+__device__ __forceinline__ double lerp_vox(wide_t<T> c0, wide_t<T> c1, double t) {
     if constexpr (VoxelBits<T>::integral) {
         const double f0 = u2d((uint32_t)c0);
         const double d = biased2d((uint32_t)c1 - (uint32_t)c0 + 0x80000000u);
@@ -265,11 +312,10 @@ __device__ __forceinline__ bool locate(const Vol<T>& v, const double p[3], Loc& 
 // sample_trilinear (_kernels.py:104-115) from a precomputed in-range Loc
 template <typename T>
 __device__ __forceinline__ double trilinear_at(const Vol<T>& v, const Loc& L) {
-    const uint32_t sx = v.sx1, sy = v.sy1, sz = v.sz1;  // L is clamped: i+1 < n unless n == 1
-    const T* b = v.data + (((uint32_t)L.k * (uint32_t)v.ny + (uint32_t)L.j) * (uint32_t)v.nx + (uint32_t)L.i);
-    const T c000 = ldv(b), c100 = ldv(b + sx), c010 = ldv(b + sy), c110 = ldv(b + sy + sx);
-    const T c001 = ldv(b + sz), c101 = ldv(b + sz + sx), c011 = ldv(b + sz + sy),
-            c111 = ldv(b + sz + sy + sx);
+    wide_t<T> c[8];  // L is clamped: i+1 < n unless n == 1
+    gather8(v, L.i, L.j, L.k, c);
+    const wide_t<T> c000 = c[0], c100 = c[1], c010 = c[2], c110 = c[3], c001 = c[4], c101 = c[5], c011 = c[6],
+                    c111 = c[7];
     const double x00 = lerp_vox<T>(c000, c100, L.fx);
     const double x10 = lerp_vox<T>(c010, c110, L.fx);
     const double x01 = lerp_vox<T>(c001, c101, L.fx);
@@ -312,7 +358,7 @@ __device__ __forceinline__ WinF make_winf(double t_low, double t_high, double am
 }
 
 template <typename T>
-__device__ __forceinline__ float vox_f32(T c) {
+__device__ __forceinline__ float vox_f32(wide_t<T> c) {
     if constexpr (VoxelBits<T>::integral) return __int_as_float(0x4B000000 | (int)c) - 8388608.0f;
     else return (float)c;
 }
@@ -320,15 +366,14 @@ __device__ __forceinline__ float vox_f32(T c) {
 template <typename T>
 __device__ __forceinline__ bool in_window_trilinear(const Vol<T>& v, const Loc& L, double t_low, double t_high,
                                                     const WinF& w) {
-    const uint32_t sx = v.sx1, sy = v.sy1, sz = v.sz1;  // L is clamped: i+1 < n unless n == 1
-    const T* b = v.data + (((uint32_t)L.k * (uint32_t)v.ny + (uint32_t)L.j) * (uint32_t)v.nx + (uint32_t)L.i);
-    const T c000 = ldv(b), c100 = ldv(b + sx), c010 = ldv(b + sy), c110 = ldv(b + sy + sx);
-    const T c001 = ldv(b + sz), c101 = ldv(b + sz + sx), c011 = ldv(b + sz + sy),
-            c111 = ldv(b + sz + sy + sx);
+    wide_t<T> c[8];  // L is clamped: i+1 < n unless n == 1
+    gather8(v, L.i, L.j, L.k, c);
+    const wide_t<T> c000 = c[0], c100 = c[1], c010 = c[2], c110 = c[3], c001 = c[4], c101 = c[5], c011 = c[6],
+                    c111 = c[7];
     const float fx = __double2float_rn(L.fx), fy = __double2float_rn(L.fy), fz = __double2float_rn(L.fz);
     auto l32 = [](float a, float bb, float t) { return __fmaf_rn(bb - a, t, a); };
-    const float y0 = l32(l32(vox_f32(c000), vox_f32(c100), fx), l32(vox_f32(c010), vox_f32(c110), fx), fy);
-    const float y1 = l32(l32(vox_f32(c001), vox_f32(c101), fx), l32(vox_f32(c011), vox_f32(c111), fx), fy);
+    const float y0 = l32(l32(vox_f32<T>(c000), vox_f32<T>(c100), fx), l32(vox_f32<T>(c010), vox_f32<T>(c110), fx), fy);
+    const float y1 = l32(l32(vox_f32<T>(c001), vox_f32<T>(c101), fx), l32(vox_f32<T>(c011), vox_f32<T>(c111), fx), fy);
     const float v32 = l32(y0, y1, fz);
     if (v32 < w.lo_out || v32 > w.hi_out) return false;
     if (v32 >= w.lo_in && v32 <= w.hi_in) return true;

@@ -85,6 +85,15 @@ def main():
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
+        stage = np.zeros(2)
+        sms = (ctypes.c_float * 2)()
+        for i in range(a.frames):  # per-stage device time (events between the two kernels)
+            P = params(10 + i)
+            flush.zero_()
+            _native.check(L.vc_render_profiled(dv.handle, ctypes.byref(P), ctypes.c_void_p(out.data_ptr()),
+                                               None, sp, sms))
+            stage += np.array([sms[0], sms[1]])
+        stage /= a.frames
         P = params(10)
         _native.check(L.vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(out.data_ptr()),
                                   ctypes.c_void_p(cnt.data_ptr()), sp))
@@ -98,7 +107,7 @@ def main():
             ref_img, ref_mode = img, mode
         t = np.array(times)
         print(f"{name:28s} {t.mean():7.3f} ms (min {t.min():.3f}, max {t.max():.3f})  "
-              f"fps {1000 / t.mean():7.1f}  samples {c[0]/1e6:6.2f}M shades {c[1]/1e6:5.2f}M "
+              f"fps {1000 / t.mean():7.1f}  stages {stage[0]:.3f}+{stage[1]:.3f}  samples {c[0]/1e6:6.2f}M shades {c[1]/1e6:5.2f}M "
               f"skip-events {c[2]/1e6:6.1f}M st1 {c[4]/1e6:6.2f}M st2 {c[5]/1e6:6.2f}M{diff}", flush=True)
 
 
