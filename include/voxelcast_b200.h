@@ -205,9 +205,10 @@ VC_API int vc_render(vc_volume *vol, const vc_render_params *p, uint8_t *d_rgba,
  * NVLink with vc_ipc_open -- at its image row.  d_frames is a device array
  * of n_frames device pointers.  After every rank's call has completed (host
  * barrier) all frame buffers hold the whole frame; replaces the separate
- * NCCL all-gather of packed bands. */
+ * NCCL all-gather of packed bands.  frame_bytes: the size of every buffer
+ * (>= height * width * 4, else VC_ERR_INVALID). */
 VC_API int vc_render_to_peers(vc_volume *vol, const vc_render_params *p, void *const *d_frames,
-                              int n_frames, uint64_t *d_counters, void *stream);
+                              int n_frames, size_t frame_bytes, uint64_t *d_counters, void *stream);
 /* Frame buffers shared across processes must be whole allocations (an IPC
  * handle maps the allocation base): allocate them here. */
 VC_API int vc_device_alloc(int device, size_t bytes, void **d_ptr);

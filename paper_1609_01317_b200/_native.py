@@ -131,7 +131,7 @@ def load(build_if_missing: bool = True):
             "vc_render": ([vp, ctypes.POINTER(RenderParams), vp, vp, vp], ctypes.c_int),
             "vc_render_profiled": ([vp, ctypes.POINTER(RenderParams), vp, vp, vp,
                                     ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
-            "vc_render_to_peers": ([vp, ctypes.POINTER(RenderParams), vp, ctypes.c_int, vp, vp],
+            "vc_render_to_peers": ([vp, ctypes.POINTER(RenderParams), vp, ctypes.c_int, ctypes.c_size_t, vp, vp],
                                    ctypes.c_int),
             "vc_device_alloc": ([ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(vp)], ctypes.c_int),
             "vc_device_free": ([vp], ctypes.c_int),
@@ -157,6 +157,9 @@ def load(build_if_missing: bool = True):
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = res
+        if hasattr(L, "vc_checked_violations"):  # the bounds-checked variant (_lib/checked)
+            L.vc_checked_violations.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+            L.vc_checked_violations.restype = ctypes.c_ulonglong
         if L.vc_render_params_size() != ctypes.sizeof(RenderParams):
             raise NativeError("vc_render_params layout mismatch between header and binding")
         _lib = L

@@ -13,6 +13,7 @@
 // a single kernel launch.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -48,6 +49,7 @@ struct vc_volume {
     cudaArray_t val_arr = nullptr, grad_arr[3] = {nullptr, nullptr, nullptr};
     cudaTextureObject_t val_tex = 0, grad_tex[3] = {0, 0, 0};
     vc::OctDev oct{};  // device octree for adaptive stepping (owned buffers)
+    long long oct_n_ivl = 0, oct_n_boxes = 0;  // its array sizes (checked builds' regions)
     uint8_t* d_scratch = nullptr;
     size_t scratch_bytes = 0;
     uint64_t* d_counters = nullptr;
@@ -400,9 +402,21 @@ int validate_params(const vc_render_params* p, int* local_rows) {
     return VC_OK;
 }
 
+// The byte ranges a launch may touch (VC_CHECKED builds upload them; the
+// kernels count and skip any access outside).  Peer frames are read back
+// from the device table.
+struct Regions {
+    std::vector<unsigned long long> lohi;
+    void add(const void* p, size_t bytes) {
+        if (!p || !bytes) return;
+        lohi.push_back((unsigned long long)p);
+        lohi.push_back((unsigned long long)p + bytes);
+    }
+};
+
 int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64_t* d_counters,
                 cudaStream_t s, int local_rows, cudaEvent_t* stage_events = nullptr,
-                void* const* d_peers = nullptr, int npeers = 0) {
+                void* const* d_peers = nullptr, int npeers = 0, size_t peer_bytes = 0) {
     vc::RenderLaunch L{};
     L.peers = d_peers;
     L.npeers = npeers;
@@ -495,6 +509,36 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
     }
     if (d_counters) VC_CUDA(cudaMemsetAsync(d_counters, 0, VC_NUM_COUNTERS * sizeof(uint64_t), s));
     if (local_rows == 0) return VC_OK;
+#ifdef VC_CHECKED
+    Regions R;
+    R.add(v->d_data, v->bytes + vc::VC_VOLUME_PAD);
+    if (L.grad) R.add(L.grad, (size_t)v->nx * v->ny * v->nz * sizeof(float4));
+    if (L.occ) R.add(L.occ, (size_t)v->mx * v->my * v->mz);
+    R.add(L.work, vc::frame_work_bytes());
+    // negative control of the checker itself (tests/test_checked_gpu.py):
+    // leave the hit queue out and every queue access must be reported
+    if (!getenv("VC_CHECKED_DROP_QUEUE")) R.add(L.hits, scp->hit_cap * vc::hit_entry_bytes());
+    R.add(d_counters, VC_NUM_COUNTERS * sizeof(uint64_t));
+    if (d_rgba) R.add(d_rgba, (size_t)local_rows * p->width * 4);
+    if (npeers > 0) {
+        R.add(d_peers, (size_t)npeers * sizeof(void*));
+        std::vector<void*> hp(npeers);
+        VC_CUDA(cudaMemcpy(hp.data(), d_peers, npeers * sizeof(void*), cudaMemcpyDeviceToHost));
+        for (void* q : hp) R.add(q, peer_bytes);
+    }
+    if (v->oct.levels > 0) {
+        const size_t lv = (size_t)v->oct.levels;
+        R.add(v->oct.dims, lv * 3 * sizeof(int32_t));
+        R.add(v->oct.amap, lv * (size_t)(v->nx + v->ny + v->nz) * sizeof(int32_t));
+        R.add(v->oct.ivl_off, lv * 3 * sizeof(int32_t));
+        R.add(v->oct.ivl, (size_t)v->oct_n_ivl * sizeof(int32_t));
+        R.add(v->oct.box_off, lv * sizeof(int64_t));
+        R.add(v->oct.state, (size_t)v->oct_n_boxes);
+        R.add(v->oct.srange, (size_t)v->oct_n_boxes * 2 * sizeof(double));
+    }
+    L.regions = R.lohi.data();
+    L.nregions = (int)(R.lohi.size() / 2);
+#endif
     VC_CUDA(vc::launch_raycast(L, s));
     VC_CUDA(cudaEventRecord(scp->done, s));
     return VC_OK;
@@ -505,6 +549,17 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
 extern "C" {
 
 int vc_abi_version(void) { return VC_ABI_VERSION; }
+
+#ifdef VC_CHECKED
+// checked builds only (not in the public header): accesses outside the
+// launches' regions since the last call, and the first offending address
+VC_API unsigned long long vc_checked_violations(unsigned long long* first) {
+    unsigned long long f1 = 0, f2 = 0;
+    const unsigned long long a = vc::vc_take_violations_raycast(&f1), b = vc::vc_take_violations_points(&f2);
+    if (first) *first = a ? f1 : f2;
+    return a + b;
+}
+#endif
 int vc_render_params_size(void) { return (int)sizeof(vc_render_params); }
 const char* vc_last_error(void) { return g_err.c_str(); }
 
@@ -565,6 +620,8 @@ int vc_volume_set_octree(vc_volume* vol, const vc_octree_desc* d) {
         return cuda_fail(e, "octree upload");
     }
     vol->oct.levels = d->levels;
+    vol->oct_n_ivl = d->n_ivl;
+    vol->oct_n_boxes = d->n_boxes;
     return VC_OK;
 }
 
@@ -611,15 +668,19 @@ int vc_render(vc_volume* vol, const vc_render_params* p, uint8_t* d_rgba, uint64
 }
 
 int vc_render_to_peers(vc_volume* vol, const vc_render_params* p, void* const* d_frames, int n_frames,
-                       uint64_t* d_counters, void* stream) {
+                       size_t frame_bytes, uint64_t* d_counters, void* stream) {
     if (!vol || !d_frames || n_frames < 1 || n_frames > 64) return fail(VC_ERR_INVALID, "need 1..64 frame buffers");
     int local_rows = 0;
     int rc = validate_params(p, &local_rows);
     if (rc) return rc;
+    // every rank's frame is stored at image_row * width + px: each buffer
+    // must hold the whole (height, width, 4) frame
+    if (frame_bytes < (size_t)p->height * p->width * 4)
+        return fail(VC_ERR_INVALID, "peer frame buffers are smaller than height * width * 4 bytes");
     DeviceGuard g(vol->device);
     std::lock_guard<std::mutex> lk(vol->mu);
     return render_impl(vol, p, nullptr, d_counters, static_cast<cudaStream_t>(stream), local_rows, nullptr,
-                       d_frames, n_frames);
+                       d_frames, n_frames, frame_bytes);
 }
 
 int vc_device_alloc(int device, size_t bytes, void** d_ptr) {
@@ -732,6 +793,25 @@ struct DevBuf {
 
 }  // namespace
 
+#ifdef VC_CHECKED
+// point kernels: the volume (their vc_device.cuh reads) is the checked region
+int point_regions(const vc_volume* vol) {
+    Regions R;
+    R.add(vol->d_data, vol->bytes + vc::VC_VOLUME_PAD);
+    VC_CUDA(vc::vc_set_regions_points(R.lohi.data(), (int)(R.lohi.size() / 2), 0));
+    return VC_OK;
+}
+#define VC_POINT_REGIONS(vol)           \
+    do {                                \
+        int _rc = point_regions(vol);   \
+        if (_rc) return _rc;            \
+    } while (0)
+#else
+#define VC_POINT_REGIONS(vol) \
+    do {                      \
+    } while (0)
+#endif
+
 int vc_sample_points(const vc_volume* vol, int interp, const double* h_pts, int64_t n, double* h_out) {
     if (!vol || (n > 0 && (!h_pts || !h_out))) return fail(VC_ERR_INVALID, "null argument");
     if (interp < 0 || interp > 2) return fail(VC_ERR_INVALID, "interp must be 0, 1 or 2");
@@ -741,6 +821,7 @@ int vc_sample_points(const vc_volume* vol, int interp, const double* h_pts, int6
     VC_CUDA(cudaMalloc(&dp.p, n * 3 * sizeof(double)));
     VC_CUDA(cudaMalloc(&dout.p, n * sizeof(double)));
     VC_CUDA(cudaMemcpy(dp.p, h_pts, n * 3 * sizeof(double), cudaMemcpyHostToDevice));
+    VC_POINT_REGIONS(vol);
     VC_CUDA(vc::launch_sample_points(vol->dtype, vol->d_data, vol->nx, vol->ny, vol->nz, interp,
                                      (const double*)dp.p, n, (double*)dout.p, 0));
     VC_CUDA(cudaMemcpy(h_out, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost));
@@ -756,6 +837,7 @@ int vc_gradient_points(const vc_volume* vol, int op, const double* h_pts, int64_
     VC_CUDA(cudaMalloc(&dp.p, n * 3 * sizeof(double)));
     VC_CUDA(cudaMalloc(&dout.p, n * 3 * sizeof(double)));
     VC_CUDA(cudaMemcpy(dp.p, h_pts, n * 3 * sizeof(double), cudaMemcpyHostToDevice));
+    VC_POINT_REGIONS(vol);
     VC_CUDA(vc::launch_gradient_points(vol->dtype, vol->d_data, vol->nx, vol->ny, vol->nz, op,
                                        (const double*)dp.p, n, (double*)dout.p, 0));
     VC_CUDA(cudaMemcpy(h_out, dout.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost));
@@ -795,6 +877,7 @@ int vc_first_hit_rays(const vc_volume* vol, const double* h_rays, int64_t n, dou
     VC_CUDA(cudaMalloc(&dc.p, sizeof(unsigned long long)));
     VC_CUDA(cudaMemset(dc.p, 0, sizeof(unsigned long long)));
     VC_CUDA(cudaMemcpy(dr.p, h_rays, n * 8 * sizeof(double), cudaMemcpyHostToDevice));
+    VC_POINT_REGIONS(vol);
     VC_CUDA(vc::launch_first_hit_rays(vol->dtype, vol->d_data, vol->nx, vol->ny, vol->nz, make_raypos(vol),
                                       (const double*)dr.p, n, coarse, fine, t_low, t_high, interp,
                                       (double*)dout.p, (unsigned long long*)dc.p, 0));
@@ -816,6 +899,7 @@ int vc_bisect_rays(const vc_volume* vol, const double* h_rays, int64_t n, double
     VC_CUDA(cudaMalloc(&dc.p, sizeof(unsigned long long)));
     VC_CUDA(cudaMemset(dc.p, 0, sizeof(unsigned long long)));
     VC_CUDA(cudaMemcpy(dr.p, h_rays, n * 8 * sizeof(double), cudaMemcpyHostToDevice));
+    VC_POINT_REGIONS(vol);
     VC_CUDA(vc::launch_bisect_rays(vol->dtype, vol->d_data, vol->nx, vol->ny, vol->nz, make_raypos(vol),
                                    (const double*)dr.p, n, t_low, t_high, iters, interp, (double*)dout.p,
                                    (unsigned long long*)dc.p, 0));

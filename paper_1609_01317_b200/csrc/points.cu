@@ -133,6 +133,10 @@ static inline unsigned blocks_for(int64_t n) { return (unsigned)((n + 127) / 128
         }                                          \
     }
 
+#ifdef VC_CHECKED
+VC_CHECKED_HOST_API(points)
+#endif
+
 cudaError_t launch_sample_points(int dtype, const void* data, int nx, int ny, int nz, int interp,
                                  const double* pts, int64_t n, double* out, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;

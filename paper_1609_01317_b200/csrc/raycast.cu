@@ -151,7 +151,7 @@ __device__ __forceinline__ int march_sample(const Ctx<T>& C, const vc_render_par
         if (C.sk.on) {
             Loc L;
             locate(C.v, p, L);
-            const int d = __ldg(C.sk.dist + macro_index(C.sk, L));
+            const int d = vc_ldg(C.sk.dist + macro_index(C.sk, L));
             if (d != 0) {
                 const int c[3] = {L.i, L.j, L.k};
                 const double kn = skip_to(t, k, base, C.sk, p, c, d);
@@ -170,7 +170,7 @@ __device__ __forceinline__ int march_sample(const Ctx<T>& C, const vc_render_par
             nskip += 1;
             return -1;
         }
-        const int d = __ldg(C.sk.dist + macro_index(C.sk, L));
+        const int d = vc_ldg(C.sk.dist + macro_index(C.sk, L));
         if (d != 0) {
             const int c[3] = {L.i, L.j, L.k};
             const double kn = skip_to(t, k, base, C.sk, p, c, d);
@@ -224,9 +224,9 @@ __device__ __forceinline__ double w_to_double(float w) {
 template <typename T, int OP>
 __device__ __noinline__ float4 gv_refine(const float4* __restrict__ b, uint32_t sy, uint32_t sz, double fx,
                                          double fy, double fz, float M) {
-    const float4 c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + sy), c110 = __ldg(b + sy + 1);
-    const float4 c001 = __ldg(b + sz), c101 = __ldg(b + sz + 1), c011 = __ldg(b + sz + sy),
-                 c111 = __ldg(b + sz + sy + 1);
+    const float4 c000 = vc_ldg(b), c100 = vc_ldg(b + 1), c010 = vc_ldg(b + sy), c110 = vc_ldg(b + sy + 1);
+    const float4 c001 = vc_ldg(b + sz), c101 = vc_ldg(b + sz + 1), c011 = vc_ldg(b + sz + sy),
+                 c111 = vc_ldg(b + sz + sy + 1);
     double h[3];
 #define VC_TRID(comp)                                                                                        \
     lerp(lerp(lerp((double)c000.comp, (double)c100.comp, fx), lerp((double)c010.comp, (double)c110.comp, fx), \
@@ -272,9 +272,9 @@ __device__ __forceinline__ bool grad_from_volume(const float4* __restrict__ G, i
     const uint32_t sy = (uint32_t)nx, sz = (uint32_t)nx * (uint32_t)ny;
     const float4* b = G + (((uint32_t)k0 * (uint32_t)ny + (uint32_t)j0) * (uint32_t)nx + (uint32_t)i0);
     cell = b;
-    const float4 c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + sy), c110 = __ldg(b + sy + 1);
-    const float4 c001 = __ldg(b + sz), c101 = __ldg(b + sz + 1), c011 = __ldg(b + sz + sy),
-                 c111 = __ldg(b + sz + sy + 1);
+    const float4 c000 = vc_ldg(b), c100 = vc_ldg(b + 1), c010 = vc_ldg(b + sy), c110 = vc_ldg(b + sy + 1);
+    const float4 c001 = vc_ldg(b + sz), c101 = vc_ldg(b + sz + 1), c011 = vc_ldg(b + sz + sy),
+                 c111 = vc_ldg(b + sz + sy + 1);
     const float ffx = (float)fx, ffy = (float)fy, ffz = (float)fz;
 #define VC_LF(a, b, t) fmaf((b) - (a), (t), (a))
 #define VC_TRIF(comp)                                                                          \
@@ -509,9 +509,9 @@ __device__ __forceinline__ bool oct_node_interval(const OctDev& o, int L, const 
     tmax = 1e300;
 #pragma unroll
     for (int a = 0; a < 3; a++) {
-        const int* iv = o.ivl + __ldg(o.ivl_off + 3 * L + a) + 2 * b[a];
-        const double lo = dmul(u2d((uint32_t)__ldg(iv)), s3[a]);  // exact, FP64 pipe
-        const double hi = dmul(u2d((uint32_t)__ldg(iv + 1)), s3[a]);
+        const int* iv = o.ivl + vc_ldg(o.ivl_off + 3 * L + a) + 2 * b[a];
+        const double lo = dmul(u2d((uint32_t)vc_ldg(iv)), s3[a]);  // exact, FP64 pipe
+        const double hi = dmul(u2d((uint32_t)vc_ldg(iv + 1)), s3[a]);
         const double ov = ov3[a], d = d3[a];
         if (d == 0.0) {
             if (ov < lo || ov > hi) return false;
@@ -547,15 +547,15 @@ __device__ __noinline__ double adaptive_stride(const OctDev o, const StrideArgs 
     long long leaf = 0;
     for (L = 0; L < o.levels; L++) {
         const int* m = o.amap + (size_t)L * stride_map;
-        b[0] = __ldg(m + ic[0]);
-        b[1] = __ldg(m + A.nx + ic[1]);
-        b[2] = __ldg(m + A.nx + A.ny + ic[2]);
-        leaf = __ldg(o.box_off + L) +
-               ((long long)b[2] * __ldg(o.dims + 3 * L + 1) + b[1]) * __ldg(o.dims + 3 * L + 0) + b[0];
-        if (__ldg(o.state + leaf) == 2) break;
+        b[0] = vc_ldg(m + ic[0]);
+        b[1] = vc_ldg(m + A.nx + ic[1]);
+        b[2] = vc_ldg(m + A.nx + A.ny + ic[2]);
+        leaf = vc_ldg(o.box_off + L) +
+               ((long long)b[2] * vc_ldg(o.dims + 3 * L + 1) + b[1]) * vc_ldg(o.dims + 3 * L + 0) + b[0];
+        if (vc_ldg(o.state + leaf) == 2) break;
     }
     if (L == o.levels) return 1.0;  // unreachable for a well-formed tree
-    const double smin = __ldg(o.srange + 2 * leaf), smax = __ldg(o.srange + 2 * leaf + 1);
+    const double smin = vc_ldg(o.srange + 2 * leaf), smax = vc_ldg(o.srange + 2 * leaf + 1);
     if (!(dsub(smax, smin) < A.detail_eps)) return 1.0;
     double tmin, tmax;
     double inv[3];
@@ -708,11 +708,15 @@ struct PixelSink {
 __device__ __forceinline__ void put_pixel(const PixelSink& s, const vc_render_params& P, int lr, int px,
                                           uchar4 o) {
     if (s.npeers == 0) {
-        s.out[(size_t)lr * P.width + px] = o;
+        uchar4* d = s.out + (size_t)lr * P.width + px;
+        if (vc_st_ok(d, sizeof(uchar4))) *d = o;
         return;
     }
     const size_t idx = (size_t)image_row(P, lr) * P.width + px;
-    for (int r = 0; r < s.npeers; r++) s.peers[r][idx] = o;
+    for (int r = 0; r < s.npeers; r++) {
+        uchar4* d = vc_ld(s.peers + r) + idx;
+        if (vc_st_ok(d, sizeof(uchar4))) *d = o;
+    }
 }
 
 // First-hit queue entry, 48 bytes (three 128-bit accesses): the refined
@@ -772,7 +776,7 @@ __device__ __forceinline__ void commit_counters(unsigned long long* counters, in
     nshade = __reduce_add_sync(FULL, nshade);
     nskip = __reduce_add_sync(FULL, nskip);
     nhit = __reduce_add_sync(FULL, nhit);
-    if ((threadIdx.x & 31) == 0) {
+    if ((threadIdx.x & 31) == 0 && vc_st_ok(counters, VC_NUM_COUNTERS * sizeof(unsigned long long))) {
         if (nsamp) atomicAdd(counters + 0, (unsigned long long)nsamp);
         if (nsamp) atomicAdd(counters + 4 + stage, (unsigned long long)nsamp);
         if (nshade) atomicAdd(counters + 1, (unsigned long long)nshade);
@@ -789,7 +793,7 @@ __device__ __forceinline__ unsigned warp_ticket(unsigned* ctr, bool want) {
     const unsigned m = __ballot_sync(FULL, want);
     unsigned base = 0;
     const int leader = __ffs(m) - 1;
-    if (m != 0 && lane == leader) base = atomicAdd(ctr, (unsigned)__popc(m));
+    if (m != 0 && lane == leader && vc_st_ok(ctr, sizeof(unsigned))) base = atomicAdd(ctr, (unsigned)__popc(m));
     base = __shfl_sync(FULL, base, leader < 0 ? 0 : leader);
     return base + __popc(m & ((1u << lane) - 1u));
 }
@@ -877,7 +881,7 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
             e.d[2] = C.rp.d[2];
             e.pix = pack_pix(lr, px);
             e.pad = 0u;
-            hits[q] = e;
+            if (vc_st_ok(hits + q, sizeof(HitEntry))) hits[q] = e;
         }
         if (active && (R.found || R.exhausted)) {
             if (R.exhausted) put_pixel(sink, P, lr, px, bg_pixel(P));
@@ -932,15 +936,15 @@ __device__ __noinline__ int seg_step(const OctDev& o, SegWalk& W, const StrideAr
         if (ta < W.tray0) ta = W.tray0;
         if (tb > W.tray1) tb = W.tray1;
         if (tb < ta) return SEG_MORE;
-        const long long box = __ldg(o.box_off + L) +
-                              ((long long)b[2] * __ldg(o.dims + 3 * L + 1) + b[1]) * __ldg(o.dims + 3 * L + 0) + b[0];
+        const long long box = vc_ldg(o.box_off + L) +
+                              ((long long)b[2] * vc_ldg(o.dims + 3 * L + 1) + b[1]) * vc_ldg(o.dims + 3 * L + 0) + b[0];
         // a box whose padded range misses the window holds no leaf that
         // does (a child's padded box lies inside its parent's): the whole
         // subtree would emit nothing, so it is pruned without changing the
         // emitted sequence
-        const bool meets = __ldg(o.srange + 2 * box) <= t_high && __ldg(o.srange + 2 * box + 1) >= t_low;
+        const bool meets = vc_ldg(o.srange + 2 * box) <= t_high && vc_ldg(o.srange + 2 * box + 1) >= t_low;
         if (!meets) return SEG_MORE;
-        if (__ldg(o.state + box) == 2) {  // leaf
+        if (vc_ldg(o.state + box) == 2) {  // leaf
             a0 = ta;
             b0 = tb;
             return SEG_LEAF;
@@ -953,9 +957,9 @@ __device__ __noinline__ int seg_step(const OctDev& o, SegWalk& W, const StrideAr
         const int axoff[3] = {0, A.nx, A.nx + A.ny};
 #pragma unroll
         for (int a = 0; a < 3; a++) {
-            const int* iv = o.ivl + __ldg(o.ivl_off + 3 * L + a) + 2 * b[a];
-            const int lo = __ldg(iv), hi = __ldg(iv + 1);
-            c0[a] = __ldg(m + axoff[a] + lo);
+            const int* iv = o.ivl + vc_ldg(o.ivl_off + 3 * L + a) + 2 * b[a];
+            const int lo = vc_ldg(iv), hi = vc_ldg(iv + 1);
+            c0[a] = vc_ldg(m + axoff[a] + lo);
             cn[a] = hi - lo >= 2 ? 2 : 1;
         }
         // oct_node_interval is separable: a child's slab along axis a depends
@@ -972,9 +976,9 @@ __device__ __noinline__ int seg_step(const OctDev& o, SegWalk& W, const StrideAr
                 sb[a][c] = 1e300;
                 sok[a][c] = true;
                 if (c < cn[a]) {
-                    const int* iv = o.ivl + __ldg(o.ivl_off + 3 * (L + 1) + a) + 2 * (c0[a] + c);
-                    const double lo = dmul(u2d((uint32_t)__ldg(iv)), A.s[a]);
-                    const double hi = dmul(u2d((uint32_t)__ldg(iv + 1)), A.s[a]);
+                    const int* iv = o.ivl + vc_ldg(o.ivl_off + 3 * (L + 1) + a) + 2 * (c0[a] + c);
+                    const double lo = dmul(u2d((uint32_t)vc_ldg(iv)), A.s[a]);
+                    const double hi = dmul(u2d((uint32_t)vc_ldg(iv + 1)), A.s[a]);
                     const double ov = A.o[a];
                     if (A.d[a] == 0.0) {
                         sok[a][c] = !(ov < lo || ov > hi);
@@ -1198,7 +1202,7 @@ __global__ void __launch_bounds__(128) firsthit_seg_kernel(const __grid_constant
             e.d[2] = C.rp.d[2];
             e.pix = pack_pix(lr, px);
             e.pad = 0u;
-            hits[q] = e;
+            if (vc_st_ok(hits + q, sizeof(HitEntry))) hits[q] = e;
             active = false;
         }
         if (miss) {
@@ -1243,7 +1247,7 @@ __global__ void __launch_bounds__(128, GV ? VC_SHV_MINB : VC_SH_MINB) shade_kern
                 if (q >= total) {
                     done = true;
                 } else {
-                    const HitEntry e = hits[q];
+                    const HitEntry e = vc_ld(hits + q);
                     px = (int)(e.pix & 0xffffu);
                     lr = (int)(e.pix >> 16);
 #pragma unroll
@@ -1380,7 +1384,17 @@ static cudaError_t launch_dtype(const RenderLaunch& L, cudaStream_t s) {
     }
 }
 
+#ifdef VC_CHECKED
+VC_CHECKED_HOST_API(raycast)
+#endif
+
 cudaError_t launch_raycast(const RenderLaunch& L, cudaStream_t s) {
+#ifdef VC_CHECKED
+    if (L.regions) {
+        cudaError_t e = vc_set_regions_raycast(L.regions, L.nregions, s);
+        if (e != cudaSuccess) return e;
+    }
+#endif
     switch (L.dtype) {
         case VC_U8: return launch_dtype<uint8_t>(L, s);
         case VC_U16: return launch_dtype<uint16_t>(L, s);

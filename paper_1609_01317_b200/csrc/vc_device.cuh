@@ -26,6 +26,71 @@ __host__ __device__ constexpr int grad_samples(int op) { return op == VC_OP_CENT
 constexpr double INV_SQRT2 = 0x1.6a09e667f3bccp-1;  // 0.7071067811865475
 constexpr double INV_SQRT3 = 0x1.279a74590331dp-1;  // 0.5773502691896258
 
+// ---- bounds-checked build (VC_CHECKED) ------------------------------------
+// compute-sanitizer is not available on this pool, so the library has a
+// checked variant of its own (paper_1609_01317_b200/_lib/checked, built by
+// build()): every global load and store of the raycast and point kernels
+// goes through vc_ldg / vc_st_ok, which test the address against the
+// buffers the launch was given (vc_set_regions, one table per translation
+// unit) and count -- and skip -- anything outside them.  The production
+// build compiles both to plain accesses.
+#ifdef VC_CHECKED
+struct VcRegion {
+    unsigned long long lo, hi;  // [lo, hi) byte addresses
+};
+constexpr int VC_MAX_REGIONS = 96;
+static __constant__ VcRegion vc_regions[VC_MAX_REGIONS];
+static __constant__ int vc_nregions;
+static __device__ unsigned long long vc_viol_count;
+static __device__ unsigned long long vc_viol_first;
+static __device__ __noinline__ bool vc_addr_ok(const void* p, unsigned n) {
+    const unsigned long long a = reinterpret_cast<unsigned long long>(p);
+    for (int r = 0; r < vc_nregions; r++)
+        if (a >= vc_regions[r].lo && a + n <= vc_regions[r].hi) return true;
+    if (atomicAdd(&vc_viol_count, 1ull) == 0ull) vc_viol_first = a;
+    return false;
+}
+template <typename T>
+__device__ __forceinline__ T vc_ldg(const T* p) {
+    return vc_addr_ok(p, sizeof(T)) ? __ldg(p) : T{};
+}
+template <typename T>
+__device__ __forceinline__ T vc_ld(const T* p) {
+    return vc_addr_ok(p, sizeof(T)) ? *p : T{};
+}
+__device__ __forceinline__ bool vc_st_ok(const void* p, unsigned n) { return vc_addr_ok(p, n); }
+// host side, one copy per translation unit (static device symbols)
+#define VC_CHECKED_HOST_API(tu)                                                                          \
+    cudaError_t vc_set_regions_##tu(const unsigned long long* lohi, int n, cudaStream_t s) {           \
+        if (n > VC_MAX_REGIONS) n = VC_MAX_REGIONS;                                                       \
+        cudaError_t e = cudaMemcpyToSymbolAsync(vc_regions, lohi, sizeof(VcRegion) * n, 0,              \
+                                                cudaMemcpyHostToDevice, s);                              \
+        if (e == cudaSuccess)                                                                            \
+            e = cudaMemcpyToSymbolAsync(vc_nregions, &n, sizeof(int), 0, cudaMemcpyHostToDevice, s);     \
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);                                              \
+        return e;                                                                                        \
+    }                                                                                                    \
+    unsigned long long vc_take_violations_##tu(unsigned long long* first) {                            \
+        unsigned long long c = 0, f = 0, z = 0;                                                          \
+        cudaDeviceSynchronize();                                                                         \
+        cudaMemcpyFromSymbol(&c, vc_viol_count, sizeof(c));                                              \
+        cudaMemcpyFromSymbol(&f, vc_viol_first, sizeof(f));                                              \
+        cudaMemcpyToSymbol(vc_viol_count, &z, sizeof(z));                                                \
+        if (first) *first = f;                                                                           \
+        return c;                                                                                        \
+    }
+#else
+template <typename T>
+__device__ __forceinline__ T vc_ldg(const T* p) {
+    return __ldg(p);
+}
+template <typename T>
+__device__ __forceinline__ T vc_ld(const T* p) {
+    return *p;
+}
+__device__ __forceinline__ constexpr bool vc_st_ok(const void*, unsigned) { return true; }
+#endif
+
 // ---- strict float64 helpers -----------------------------------------------
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
@@ -138,14 +203,14 @@ __device__ __forceinline__ void gather8(const Vol<T>& v, int i, int j, int k, wi
     const T* p1 = reinterpret_cast<const T*>(reinterpret_cast<const char*>(p0) + v.syb);
     const T* p2 = reinterpret_cast<const T*>(reinterpret_cast<const char*>(p0) + v.szb);
     const T* p3 = reinterpret_cast<const T*>(reinterpret_cast<const char*>(p2) + v.syb);
-    c[0] = __ldg(p0);
-    c[1] = __ldg(p0 + 1);
-    c[2] = __ldg(p1);
-    c[3] = __ldg(p1 + 1);
-    c[4] = __ldg(p2);
-    c[5] = __ldg(p2 + 1);
-    c[6] = __ldg(p3);
-    c[7] = __ldg(p3 + 1);
+    c[0] = vc_ldg(p0);
+    c[1] = vc_ldg(p0 + 1);
+    c[2] = vc_ldg(p1);
+    c[3] = vc_ldg(p1 + 1);
+    c[4] = vc_ldg(p2);
+    c[5] = vc_ldg(p2 + 1);
+    c[6] = vc_ldg(p3);
+    c[7] = vc_ldg(p3 + 1);
     if (v.sx1 == 0u) {
         c[1] = c[0];
         c[3] = c[2];
@@ -155,7 +220,7 @@ __device__ __forceinline__ void gather8(const Vol<T>& v, int i, int j, int k, wi
 }
 
 template <typename T>
-__device__ __forceinline__ T ldv(const T* p) { return __ldg(p); }
+__device__ __forceinline__ T ldv(const T* p) { return vc_ldg(p); }
 
 // _kernels.py:40-42
 template <typename T>

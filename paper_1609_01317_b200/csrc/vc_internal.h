@@ -54,7 +54,17 @@ struct RenderLaunch {
     // the float4 gradient volume (0 when grad == nullptr)
     cudaTextureObject_t tex_value, tex_grad;
     float tex_scale;
+    // VC_CHECKED builds: the [lo, hi) byte ranges the launch may touch
+    const unsigned long long* regions;
+    int nregions;
 };
+
+#ifdef VC_CHECKED
+cudaError_t vc_set_regions_raycast(const unsigned long long* lohi, int n, cudaStream_t s);
+unsigned long long vc_take_violations_raycast(unsigned long long* first);
+cudaError_t vc_set_regions_points(const unsigned long long* lohi, int n, cudaStream_t s);
+unsigned long long vc_take_violations_points(unsigned long long* first);
+#endif
 
 cudaError_t launch_raycast(const RenderLaunch& L, cudaStream_t s);
 size_t hit_entry_bytes();

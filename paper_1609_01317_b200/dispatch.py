@@ -205,7 +205,7 @@ class PeerFrames:
             raise ValueError(f"frame {P.height}x{P.width} does not match the peer buffers "
                              f"{self.height}x{self.width}")
         _native.check(_native.load().vc_render_to_peers(
-            dv.handle, ctypes.byref(P), ctypes.c_void_p(self.table.data_ptr()), self.world,
+            dv.handle, ctypes.byref(P), ctypes.c_void_p(self.table.data_ptr()), self.world, self.nbytes,
             ctypes.c_void_p(counters_ptr), ctypes.c_void_p(stream_ptr)))
 
     def download(self, out: np.ndarray, stream_ptr: int = 0) -> np.ndarray:
