@@ -570,7 +570,9 @@ def run_ours(args):
     # (peer-frame validation, gathers, max-over-ranks timing, e2e) with all
     # ranks on one GPU -- a functional check, not a scaling measurement
     backend = os.environ.get("VC_BENCH_DIST_BACKEND", "nccl")
-    if "VC_BENCH_DEVICE" in os.environ:
+    # ranks sharing one GPU (functional check): device flag waits are host-ordered
+    shared_gpu = "VC_BENCH_DEVICE" in os.environ
+    if shared_gpu:
         local = int(os.environ["VC_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     dev = local
@@ -606,13 +608,14 @@ def run_ours(args):
             # frame over NVLink (two frame buffers, alternating); validated
             # against the NCCL path on one frame before use
             try:
-                peers = [PeerFrames(H, W, dev), PeerFrames(H, W, dev)]
+                peers = [PeerFrames(H, W, dev, host_ordered=shared_gpu),
+                         PeerFrames(H, W, dev, host_ordered=shared_gpu)]
                 sc, st = frame(0)
                 P = render_params(vol, sc, st, band_rows=plan.band_rows, band_first=rank, band_step=world)
                 peers[0].render(dv, P, 0, stream.cuda_stream)
-                torch.cuda.synchronize(dev)
-                torch.distributed.barrier()
-                got = peers[0].download(np.empty((H, W, 4), np.uint8))
+                peers[0].wait_frame(stream.cuda_stream)
+                got = peers[0].download(np.empty((H, W, 4), np.uint8), stream.cuda_stream)
+                peers[0].release(stream.cuda_stream)
                 _native.check(L.vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(local_buf.data_ptr()),
                                           None, sp))
                 want = gather(local_buf).cpu().numpy()
@@ -630,8 +633,11 @@ def run_ours(args):
     def render(i, counters=None):
         sc, st = frame(i)
         P = render_params(vol, sc, st, band_rows=plan.band_rows, band_first=rank, band_step=world)
-        if peers is not None:
-            peers[i & 1].render(dv, P, counters.value if counters is not None else 0, stream.cuda_stream)
+        if peers is not None:  # push this rank's tiles, wait (device-side) for everyone's, release
+            pf = peers[i & 1]
+            pf.render(dv, P, counters.value if counters is not None else 0, stream.cuda_stream)
+            pf.wait_frame(stream.cuda_stream)
+            pf.release(stream.cuda_stream)
             return None
         _native.check(L.vc_render(dv.handle, ctypes.byref(P), ctypes.c_void_p(local_buf.data_ptr()),
                                   counters, sp))
@@ -827,28 +833,40 @@ def run_ours(args):
 
     if not args.no_e2e and world > 1:
         # end to end at N GPUs through the public multi-GPU API: every step
-        # renders the rank's bands, gathers (fused peer stores or NCCL), and
-        # copies the full frame to host memory on every rank
+        # renders the rank's bands and delivers them to rank 0 (fused peer
+        # tile pushes into rank 0's frame + device completion flags, or NCCL),
+        # and rank 0 alone copies the frame to host memory; no host barrier
+        # per frame (the other ranks run ahead, bounded by the flags)
         from paper_1609_01317_b200.dispatch import render_frame_distributed
 
         gmode = "peer" if peers is not None else "nccl"
+        to0 = None
+        if peers is not None:
+            to0 = [PeerFrames(H, W, dev, dest=0, host_ordered=shared_gpu),
+                   PeerFrames(H, W, dev, dest=0, host_ordered=shared_gpu)]
         for i in range(2):
-            render_frame_distributed(vol, *frame(i), gather=gmode, peers=peers[0] if peers else None)
+            render_frame_distributed(vol, *frame(i), gather=gmode, peers=to0[i & 1] if to0 else None)
         barrier()
         t0 = time.perf_counter()
         checksum = 0
         for k in range(args.steps):
             fb = render_frame_distributed(vol, *frame(args.warmup + k), gather=gmode,
-                                          peers=peers[0] if peers else None)
-            checksum += int(fb.pixels[H // 2, W // 2, 0])
-        barrier()
+                                          peers=to0[k & 1] if to0 else None)
+            if fb is not None:
+                checksum += int(fb.pixels[H // 2, W // 2, 0])
+        torch.cuda.synchronize(dev)
         t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{dev}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        if to0 is not None:
+            torch.distributed.barrier()
+            for pf in to0:
+                pf.close()
         e2e = {"value": args.steps / float(t.item()), "unit": UNIT,
                "h2d_bytes_per_step": ctypes.sizeof(_native.RenderParams),
-               "d2h_bytes_per_step": H * W * 4 + 8 * _native.NUM_COUNTERS,
-               "path": f"paper_1609_01317_b200.dispatch.render_frame_distributed(gather={gmode!r}), "
-                       "synchronous per frame, full frame to host on every rank; wall clock, max over ranks",
+               "d2h_bytes_per_step": H * W * 4,
+               "path": f"paper_1609_01317_b200.dispatch.render_frame_distributed(gather={gmode!r}"
+                       + (", PeerFrames(dest=0)" if to0 else "") + "): frame delivered to rank 0, which "
+                       "alone copies it to host memory; no host barrier per frame; wall clock, max over ranks",
                "note": "h2d per step = the scene/camera parameter block (kernel parameters)"}
 
     if peers is not None:

@@ -38,7 +38,7 @@ extern "C" {
 #define VC_API
 #endif
 
-#define VC_ABI_VERSION 3
+#define VC_ABI_VERSION 4
 #define VC_MAX_LUT 64
 
 typedef enum {
@@ -198,17 +198,42 @@ VC_API int vc_gradient_prepass_into(const vc_volume *vol, int op, void *d_out, v
  * d_counters may be NULL. */
 VC_API int vc_render(vc_volume *vol, const vc_render_params *p, uint8_t *d_rgba, uint64_t *d_counters,
               void *stream);
-/* Image-tile render fused with the gather (multi-GPU, one process per GPU):
- * renders the bands of p (band_first / band_step) and stores every finished
- * pixel straight into each of the n_frames full (height, width, 4) frame
- * buffers -- this rank's own and the other ranks' buffers mapped over
- * NVLink with vc_ipc_open -- at its image row.  d_frames is a device array
- * of n_frames device pointers.  After every rank's call has completed (host
- * barrier) all frame buffers hold the whole frame; replaces the separate
- * NCCL all-gather of packed bands.  frame_bytes: the size of every buffer
- * (>= height * width * 4, else VC_ERR_INVALID). */
-VC_API int vc_render_to_peers(vc_volume *vol, const vc_render_params *p, void *const *d_frames,
-                              int n_frames, size_t frame_bytes, uint64_t *d_counters, void *stream);
+/* Image-tile render fused with the gather (multi-GPU, one process per GPU).
+ * Every rank owns one full (height, width, 4) frame buffer; d_frames is a
+ * device array of all ranks' buffers (this rank's own at index self, the
+ * others mapped over NVLink with vc_ipc_open).  The call renders the bands
+ * of p (band_first / band_step) and delivers them into the frame buffer of
+ * every receiving rank (dest = -1: all ranks, an all-gather; dest = r: rank
+ * r only, a gather) from inside the raycast kernels: with band_rows a
+ * multiple of 4 each finished 8x4 screen tile is pushed as 16-byte row
+ * segments, otherwise pixel by pixel.  With d_done set, a signal follows on
+ * the same stream: after a system-scope fence, d_done[r][self] = seq for
+ * every receiving rank r (release).  A receiver waits for
+ * d_done[own][0..n) >= seq with vc_wait_flags on its stream: no host
+ * barrier per frame.  Replaces the separate NCCL all-gather of packed bands
+ * (raycast.py:476-505 has one host, one pool). */
+#define VC_MAX_PEERS 64
+typedef struct vc_peer_frames {
+    void *const *d_frames;     /* device array [n] of frame buffers */
+    uint32_t *const *d_done;   /* device array [n] of "done" flag blocks (VC_MAX_PEERS slots), or NULL */
+    uint64_t frame_bytes;      /* size of every frame buffer (>= height * width * 4) */
+    int32_t n;                 /* ranks, 1..VC_MAX_PEERS */
+    int32_t self;              /* this rank's index */
+    int32_t dest;              /* -1: every rank receives the frame; r: only rank r */
+    uint32_t seq;              /* this frame's sequence number (signalled into d_done) */
+} vc_peer_frames;
+VC_API int vc_render_to_peers(vc_volume *vol, const vc_render_params *p, const vc_peer_frames *peers,
+                              uint64_t *d_counters, void *stream);
+/* Flag signal / wait of the peer protocol (also the "buffer free again"
+ * back-channel from receivers to senders).  vc_signal_flags: after a
+ * system-scope fence, blocks[r][slot] = seq for r in [0, n) (only r = dest
+ * when dest >= 0), stream-ordered.  vc_wait_flags: the stream waits until
+ * block[first .. first+count) are all >= seq (acquire, sequence numbers
+ * compared modulo 2^32); after timeout_us it gives up and writes 1 to
+ * *d_status (0 on success; d_status may be NULL). */
+VC_API int vc_signal_flags(uint32_t *const *d_blocks, int n, int dest, int slot, uint32_t seq, void *stream);
+VC_API int vc_wait_flags(const uint32_t *d_block, int first, int count, uint32_t seq, uint32_t timeout_us,
+                         int32_t *d_status, void *stream);
 /* Frame buffers shared across processes must be whole allocations (an IPC
  * handle maps the allocation base): allocate them here. */
 VC_API int vc_device_alloc(int device, size_t bytes, void **d_ptr);

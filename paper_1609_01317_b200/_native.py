@@ -37,7 +37,7 @@ EXPORTS = (
     "vc_volume_create", "vc_volume_create_device", "vc_volume_destroy", "vc_volume_data",
     "vc_volume_set_octree",
     "vc_gradient_prepass", "vc_gradient_volume", "vc_gradient_prepass_into",
-    "vc_render", "vc_render_profiled", "vc_render_host", "vc_render_to_peers",
+    "vc_render", "vc_render_profiled", "vc_render_host", "vc_render_to_peers", "vc_signal_flags", "vc_wait_flags",
     "vc_ipc_handle", "vc_ipc_open", "vc_ipc_close", "vc_device_alloc", "vc_device_free",
     "vc_memcpy_to_host", "vc_sample_peak", "vc_sample_peak_texture", "vc_encode_png",
     "vc_sample_points", "vc_gradient_points",
@@ -71,6 +71,18 @@ class RenderParams(ctypes.Structure):
         ("detail_eps", ctypes.c_double),
         ("sampler", ctypes.c_int32), ("row_end", ctypes.c_int32),
     ]
+
+
+class PeerFramesDesc(ctypes.Structure):
+    """Mirror of vc_peer_frames."""
+
+    _fields_ = [
+        ("d_frames", ctypes.c_void_p), ("d_done", ctypes.c_void_p), ("frame_bytes", ctypes.c_uint64),
+        ("n", ctypes.c_int32), ("self", ctypes.c_int32), ("dest", ctypes.c_int32), ("seq", ctypes.c_uint32),
+    ]
+
+
+MAX_PEERS = 64
 
 
 class OctreeDesc(ctypes.Structure):
@@ -131,8 +143,11 @@ def load(build_if_missing: bool = True):
             "vc_render": ([vp, ctypes.POINTER(RenderParams), vp, vp, vp], ctypes.c_int),
             "vc_render_profiled": ([vp, ctypes.POINTER(RenderParams), vp, vp, vp,
                                     ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
-            "vc_render_to_peers": ([vp, ctypes.POINTER(RenderParams), vp, ctypes.c_int, ctypes.c_size_t, vp, vp],
+            "vc_render_to_peers": ([vp, ctypes.POINTER(RenderParams), ctypes.POINTER(PeerFramesDesc), vp, vp],
                                    ctypes.c_int),
+            "vc_signal_flags": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_uint32, vp], ctypes.c_int),
+            "vc_wait_flags": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32, vp, vp],
+                              ctypes.c_int),
             "vc_device_alloc": ([ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(vp)], ctypes.c_int),
             "vc_device_free": ([vp], ctypes.c_int),
             "vc_sample_peak": ([ctypes.c_int, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),

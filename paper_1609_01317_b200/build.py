@@ -19,7 +19,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libvoxelcast_b200.so"
-SOURCES = ["capi.cu", "raycast.cu", "gradient_prepass.cu", "macrocell.cu", "points.cu", "peak.cu", "png.cu"]
+SOURCES = ["capi.cu", "raycast.cu", "gradient_prepass.cu", "macrocell.cu", "points.cu", "peak.cu", "png.cu",
+           "peer.cu"]
 HEADERS = ["vc_device.cuh", "vc_internal.h"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

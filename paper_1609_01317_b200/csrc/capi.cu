@@ -59,6 +59,8 @@ struct vc_volume {
         void* work = nullptr;
         void* hits = nullptr;
         size_t hit_cap = 0;
+        unsigned* tiles = nullptr;  // 8x4 tile counters of the peer tile pushes
+        size_t tile_cap = 0;
         cudaEvent_t done = nullptr;  // recorded after each render that used it
         uint64_t stamp = 0;
     };
@@ -205,6 +207,7 @@ void release(vc_volume* v) {
     for (auto& kv : v->scratch) {
         cudaFree(kv.second.work);
         cudaFree(kv.second.hits);
+        cudaFree(kv.second.tiles);
         if (kv.second.done) cudaEventDestroy(kv.second.done);
     }
     if (v->host_stream) cudaStreamDestroy(v->host_stream);
@@ -416,10 +419,16 @@ struct Regions {
 
 int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64_t* d_counters,
                 cudaStream_t s, int local_rows, cudaEvent_t* stage_events = nullptr,
-                void* const* d_peers = nullptr, int npeers = 0, size_t peer_bytes = 0) {
+                const vc_peer_frames* pf = nullptr) {
     vc::RenderLaunch L{};
+    void* const* d_peers = pf ? pf->d_frames : nullptr;
+    const int npeers = pf ? pf->n : 0;
+    const size_t peer_bytes = pf ? (size_t)pf->frame_bytes : 0;
     L.peers = d_peers;
     L.npeers = npeers;
+    L.peer_self = pf ? pf->self : 0;
+    L.peer_dest = pf ? pf->dest : -1;
+    L.tile_cnt = nullptr;
     if (stage_events)
         for (int i = 0; i < 3; i++) L.ev[i] = stage_events[i];
     L.p = p;
@@ -447,6 +456,7 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
             if (old->second.done) VC_CUDA(cudaEventSynchronize(old->second.done));
             cudaFree(old->second.work);
             cudaFree(old->second.hits);
+            cudaFree(old->second.tiles);
             if (old->second.done) cudaEventDestroy(old->second.done);
             v->scratch.erase(old);
         }
@@ -466,6 +476,18 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
         }
         L.work = sc.work;
         L.hits = sc.hits;
+        // tile pushes need whole 8x4 tiles inside one band (band_rows % 4 == 0)
+        if (npeers > 0 && p->band_rows % 4 == 0) {
+            const size_t tiles = (size_t)((p->width + 7) / 8) * (size_t)((local_rows + 3) / 4);
+            if (sc.tile_cap < tiles) {
+                cudaFree(sc.tiles);
+                sc.tiles = nullptr;
+                sc.tile_cap = 0;
+                VC_CUDA(cudaMalloc(&sc.tiles, tiles * sizeof(unsigned)));
+                sc.tile_cap = tiles;
+            }
+            L.tile_cnt = sc.tiles;
+        }
     }
     L.mx = v->mx;
     L.my = v->my;
@@ -525,6 +547,7 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
         std::vector<void*> hp(npeers);
         VC_CUDA(cudaMemcpy(hp.data(), d_peers, npeers * sizeof(void*), cudaMemcpyDeviceToHost));
         for (void* q : hp) R.add(q, peer_bytes);
+        if (L.tile_cnt) R.add(L.tile_cnt, scp->tile_cap * sizeof(unsigned));
     }
     if (v->oct.levels > 0) {
         const size_t lv = (size_t)v->oct.levels;
@@ -540,6 +563,8 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
     L.nregions = (int)(R.lohi.size() / 2);
 #endif
     VC_CUDA(vc::launch_raycast(L, s));
+    if (pf && pf->d_done)  // this rank's bands are in every receiver's frame
+        VC_CUDA(vc::launch_signal_flags(pf->d_done, pf->n, pf->dest, pf->self, pf->seq, s));
     VC_CUDA(cudaEventRecord(scp->done, s));
     return VC_OK;
 }
@@ -667,20 +692,37 @@ int vc_render(vc_volume* vol, const vc_render_params* p, uint8_t* d_rgba, uint64
     return render_impl(vol, p, d_rgba, d_counters, static_cast<cudaStream_t>(stream), local_rows);
 }
 
-int vc_render_to_peers(vc_volume* vol, const vc_render_params* p, void* const* d_frames, int n_frames,
-                       size_t frame_bytes, uint64_t* d_counters, void* stream) {
-    if (!vol || !d_frames || n_frames < 1 || n_frames > 64) return fail(VC_ERR_INVALID, "need 1..64 frame buffers");
+int vc_render_to_peers(vc_volume* vol, const vc_render_params* p, const vc_peer_frames* pf, uint64_t* d_counters,
+                       void* stream) {
+    if (!vol || !pf || !pf->d_frames) return fail(VC_ERR_INVALID, "null argument");
+    if (pf->n < 1 || pf->n > VC_MAX_PEERS) return fail(VC_ERR_INVALID, "need 1..VC_MAX_PEERS frame buffers");
+    if (pf->self < 0 || pf->self >= pf->n || pf->dest < -1 || pf->dest >= pf->n)
+        return fail(VC_ERR_INVALID, "self / dest out of range");
     int local_rows = 0;
     int rc = validate_params(p, &local_rows);
     if (rc) return rc;
-    // every rank's frame is stored at image_row * width + px: each buffer
+    // every receiver's frame is stored at image_row * width + px: each buffer
     // must hold the whole (height, width, 4) frame
-    if (frame_bytes < (size_t)p->height * p->width * 4)
+    if (pf->frame_bytes < (uint64_t)p->height * p->width * 4)
         return fail(VC_ERR_INVALID, "peer frame buffers are smaller than height * width * 4 bytes");
     DeviceGuard g(vol->device);
     std::lock_guard<std::mutex> lk(vol->mu);
-    return render_impl(vol, p, nullptr, d_counters, static_cast<cudaStream_t>(stream), local_rows, nullptr,
-                       d_frames, n_frames, frame_bytes);
+    return render_impl(vol, p, nullptr, d_counters, static_cast<cudaStream_t>(stream), local_rows, nullptr, pf);
+}
+
+int vc_signal_flags(uint32_t* const* d_blocks, int n, int dest, int slot, uint32_t seq, void* stream) {
+    if (!d_blocks || n < 1 || n > VC_MAX_PEERS || slot < 0 || slot >= VC_MAX_PEERS || dest < -1 || dest >= n)
+        return fail(VC_ERR_INVALID, "bad flag-block arguments");
+    VC_CUDA(vc::launch_signal_flags(d_blocks, n, dest, slot, seq, static_cast<cudaStream_t>(stream)));
+    return VC_OK;
+}
+
+int vc_wait_flags(const uint32_t* d_block, int first, int count, uint32_t seq, uint32_t timeout_us, int32_t* d_status,
+                  void* stream) {
+    if (!d_block || first < 0 || count < 0 || first + count > VC_MAX_PEERS)
+        return fail(VC_ERR_INVALID, "bad flag-block arguments");
+    VC_CUDA(vc::launch_wait_flags(d_block, first, count, seq, timeout_us, d_status, static_cast<cudaStream_t>(stream)));
+    return VC_OK;
 }
 
 int vc_device_alloc(int device, size_t bytes, void** d_ptr) {

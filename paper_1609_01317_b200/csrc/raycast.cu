@@ -694,16 +694,59 @@ __device__ __forceinline__ bool shade_and_composite(const Ctx<T>& C, const vc_re
 constexpr int READY_DEN = 4;
 
 // Where finished pixels go: the packed local rows of this rank (npeers == 0)
-// or, fused with the image-tile gather, every rank's full frame buffer over
-// NVLink peer mappings (npeers > 0): each pixel is stored once per
-// destination straight from the kernel that finished it, so the frame is
-// assembled on all GPUs when the kernels and a host barrier complete -- no
-// separate all-gather pass.
+// or, fused with the image-tile gather, the full frame buffers of the ranks
+// (npeers > 0: a device table of every rank's frame, this rank's own local,
+// the others mapped over NVLink).  With tile counters (band_rows a multiple
+// of 4, so an 8x4 screen tile never straddles two bands) a pixel goes to the
+// rank's own frame first; the lane that completes a tile -- its pixels come
+// from both kernels, in any order -- pushes the tile's four 32-byte rows to
+// the receiving ranks as 16-byte stores (two per row per receiver) instead
+// of one 4-byte remote store per pixel per receiver.  dest >= 0 sends to one
+// rank only (a gather to that rank), -1 to every rank.
 struct PixelSink {
     uchar4* out;
     uchar4* const* peers;
     int npeers;
+    int self, dest;
+    unsigned* tile_cnt;  // zeroed per frame; nullptr: per-pixel remote stores
+    int tiles_x, local_rows;
 };
+
+__device__ __forceinline__ bool sink_receives(const PixelSink& s, int r) { return s.dest < 0 || r == s.dest; }
+
+// the completed tile (local rows lr0.., columns x0..) from this rank's frame to
+// the receiving ranks; its pixels were written and fenced by any thread of
+// either kernel, so they are read through L2 (ld.global.cg)
+__device__ __noinline__ void push_tile(const PixelSink s, const vc_render_params& P, int lr0, int x0) {
+    const int W = P.width;
+    const int nr = min(4, s.local_rows - lr0), nc = min(8, W - x0);
+    const uchar4* own = vc_ld(s.peers + s.self);
+    const bool vec = nc == 8 && (W & 3) == 0;  // 16-byte aligned 32-byte rows
+    for (int r = 0; r < nr; r++) {
+        const size_t base = (size_t)image_row(P, lr0 + r) * W + x0;
+        if (vec) {
+            const uint4* src = reinterpret_cast<const uint4*>(own + base);
+            const uint4 a = __ldcg(src), b = __ldcg(src + 1);
+            for (int q = 0; q < s.npeers; q++) {
+                if (q == s.self || !sink_receives(s, q)) continue;
+                uint4* dst = reinterpret_cast<uint4*>(vc_ld(s.peers + q) + base);
+                if (vc_st_ok(dst, 32)) {
+                    dst[0] = a;
+                    dst[1] = b;
+                }
+            }
+        } else {
+            for (int c = 0; c < nc; c++) {
+                const unsigned v = __ldcg(reinterpret_cast<const unsigned*>(own + base + c));
+                for (int q = 0; q < s.npeers; q++) {
+                    if (q == s.self || !sink_receives(s, q)) continue;
+                    unsigned* dst = reinterpret_cast<unsigned*>(vc_ld(s.peers + q) + base + c);
+                    if (vc_st_ok(dst, 4)) *dst = v;
+                }
+            }
+        }
+    }
+}
 
 __device__ __forceinline__ void put_pixel(const PixelSink& s, const vc_render_params& P, int lr, int px,
                                           uchar4 o) {
@@ -713,9 +756,23 @@ __device__ __forceinline__ void put_pixel(const PixelSink& s, const vc_render_pa
         return;
     }
     const size_t idx = (size_t)image_row(P, lr) * P.width + px;
-    for (int r = 0; r < s.npeers; r++) {
-        uchar4* d = vc_ld(s.peers + r) + idx;
-        if (vc_st_ok(d, sizeof(uchar4))) *d = o;
+    if (s.tile_cnt == nullptr) {  // one store per pixel per receiving rank
+        for (int r = 0; r < s.npeers; r++) {
+            if (r != s.self && !sink_receives(s, r)) continue;
+            uchar4* d = vc_ld(s.peers + r) + idx;
+            if (vc_st_ok(d, sizeof(uchar4))) *d = o;
+        }
+        return;
+    }
+    uchar4* d = vc_ld(s.peers + s.self) + idx;
+    if (vc_st_ok(d, sizeof(uchar4))) *d = o;
+    __threadfence();  // the pixel is visible before it is counted
+    const int lr0 = lr & ~3, x0 = px & ~7;
+    const unsigned need = (unsigned)(min(8, P.width - x0) * min(4, s.local_rows - lr0));
+    unsigned* cnt = s.tile_cnt + (size_t)(lr0 >> 2) * s.tiles_x + (x0 >> 3);
+    if (vc_st_ok(cnt, sizeof(unsigned)) && atomicAdd(cnt, 1u) + 1u == need) {
+        __threadfence();  // every counted pixel is visible to the pushing lane
+        push_tile(s, P, lr0, x0);
     }
 }
 
@@ -1326,7 +1383,12 @@ static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
     cudaError_t e = cudaMemsetAsync(fw, 0, sizeof(FrameWork), stream);
     if (e != cudaSuccess) return e;
     const long long tiles = (long long)((L.p->width + 7) / 8) * ((L.local_rows + 3) / 4);
-    PixelSink sink{reinterpret_cast<uchar4*>(L.out), reinterpret_cast<uchar4* const*>(L.peers), L.npeers};
+    PixelSink sink{reinterpret_cast<uchar4*>(L.out), reinterpret_cast<uchar4* const*>(L.peers), L.npeers,
+                   L.peer_self, L.peer_dest, L.tile_cnt, (L.p->width + 7) / 8, L.local_rows};
+    if (L.tile_cnt != nullptr) {
+        e = cudaMemsetAsync(L.tile_cnt, 0, sizeof(unsigned) * (size_t)tiles, stream);
+        if (e != cudaSuccess) return e;
+    }
     TexArgs tex{L.tex_value, L.tex_grad, L.tex_scale, 0.0f, 0.0f};
     // v >= t_low <=> v >= RU(t_low) for a float v (and v <= t_high <=> v <= RD(t_high))
     tex.lo = (float)L.p->t_low;

@@ -43,6 +43,8 @@ struct RenderLaunch {
     uint8_t* out;         // local_rows x width x 4 (npeers == 0)
     void* const* peers;   // device array of npeers full-frame buffers (fused gather)
     int npeers;
+    int peer_self, peer_dest;  // this rank's own buffer in peers; receiving rank (-1: all)
+    unsigned* tile_cnt;        // 8x4 tile completion counters (peer tile pushes) or nullptr
     int local_rows;
     uint64_t* counters;   // VC_NUM_COUNTERS or nullptr
     void* work;           // frame work counters (FrameWork, zeroed per launch)
@@ -84,6 +86,11 @@ cudaError_t launch_macrocell_minmax(int dtype, const void* data, int nx, int ny,
 constexpr int DIST_PASSES = VC_DIST_PASSES;  // max jump = (DIST_PASSES + 1) macrocells
 cudaError_t launch_occupancy(const float2* mm, int mx, int my, int mz, double lo, double hi, uint8_t* dist,
                              uint8_t* scratch, cudaStream_t s);
+
+// device completion flags of the peer gather (peer.cu)
+cudaError_t launch_signal_flags(uint32_t* const* blocks, int n, int dest, int slot, uint32_t seq, cudaStream_t s);
+cudaError_t launch_wait_flags(const uint32_t* block, int first, int count, uint32_t seq, uint32_t timeout_us,
+                              int32_t* status, cudaStream_t s);
 
 // point queries (points.cu)
 cudaError_t launch_sample_points(int dtype, const void* data, int nx, int ny, int nz, int interp,

@@ -80,11 +80,14 @@ def render_frame_distributed(volume: Volume, scene: Scene, settings: RenderSetti
                              *, band_rows: int = 8, group=None, gather: str = "nccl",
                              peers: "PeerFrames | None" = None) -> FrameBuffer | None:
     """render_frame across all ranks of the default process group (one GPU
-    per rank, LOCAL_RANK = device).  Every rank gets the full frame back.
+    per rank, LOCAL_RANK = device).
 
-    gather="nccl": packed bands + NCCL all-gather (TileGather);
-    gather="peer": the fused path (PeerFrames, created on first use unless
-    passed in), pixels stored over NVLink by the raycast kernels."""
+    gather="nccl": packed bands + NCCL all-gather (TileGather); every rank
+    gets the full frame.  gather="peer": the fused path (PeerFrames, created
+    on first use unless passed in): the raycast kernels push finished tiles
+    over NVLink into the receiving ranks' frames and signal device-side
+    completion flags; a receiver's stream waits on them -- no host barrier
+    per frame.  Ranks that do not receive (PeerFrames(dest=r)) return None."""
     import time
 
     import torch
@@ -105,14 +108,19 @@ def render_frame_distributed(volume: Volume, scene: Scene, settings: RenderSetti
             peers = PeerFrames(settings.height, settings.width, dev, group)
         t0 = time.perf_counter()
         peers.render(dv, P, cnt.data_ptr(), stream.cuda_stream)
-        torch.cuda.synchronize(dev)
-        dist.barrier(group=group)  # every rank's stores have landed in every buffer
-        pixels = peers.download(np.empty((settings.height, settings.width, 4), np.uint8))
+        pixels = None
+        if peers.receives:
+            peers.wait_frame(stream.cuda_stream)
+            pixels = peers.download(np.empty((settings.height, settings.width, 4), np.uint8), stream.cuda_stream)
+            peers.release(stream.cuda_stream)
         ms = (time.perf_counter() - t0) * 1000.0
         dist.all_reduce(cnt, group=group)
         if own:
-            dist.barrier(group=group)  # nobody still reads a mapping we are about to unmap
+            torch.cuda.synchronize(dev)
+            dist.barrier(group=group)  # nobody still writes into a mapping we are about to unmap
             peers.close()
+        if pixels is None:
+            return None
         c = cnt.cpu().numpy()
         return FrameBuffer(settings.width, settings.height, pixels, ms, sample_count_of(c, P.op))
     if gather != "nccl":
@@ -159,20 +167,47 @@ class _NativeIpc:
         self.L.vc_ipc_close(ctypes.c_void_p(ptr))
 
 
-class PeerFrames:
-    """Fused image-tile gather over NVLink peer memory.
+class _DeviceBytes:
+    """A raw device allocation seen by torch (zeroing, views) through the
+    CUDA array interface."""
 
-    Every rank owns one full (H, W, 4) frame buffer allocated as its own
-    cudaMalloc block; the IPC handles are exchanged once (all_gather_object
-    over the process group) and every rank maps every other rank's buffer.
-    vc_render_to_peers then stores each finished pixel into all ranks'
-    buffers from inside the raycast kernels, so after the kernels and one
-    host barrier every GPU holds the whole frame -- the compute and the
-    collective are one pass (the NCCL all-gather path, TileGather, is the
-    baseline it replaces).
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class PeerFrames:
+    """Fused image-tile gather over NVLink peer memory, with device-side
+    completion flags.
+
+    Every rank owns one IPC allocation: its full (H, W, 4) frame buffer and
+    two flag blocks of MAX_PEERS uint32 slots -- "done" (slot r: the last
+    frame sequence number rank r finished storing into this frame) and
+    "free" (slot c: the last frame receiver c finished reading from this
+    rank's targets).  Handles are exchanged once (all_gather_object); every
+    rank maps every other rank's allocation.  Per frame, with no host
+    synchronisation:
+
+      render()      sender: its stream waits until every receiver released
+                    the previous use of this buffer pair ("free" >= seq - 1),
+                    then vc_render_to_peers pushes its bands into the
+                    receivers' frames and raises their "done" slot
+      wait_frame()  receiver: its stream waits for all "done" slots >= seq
+      release()     receiver, after reading: raises its slot in every
+                    sender's "free" block
+
+    dest=None: every rank receives the frame (all-gather); dest=r: rank r
+    only (a gather; the other ranks' streams never wait).  host_ordered=True
+    (ranks sharing ONE GPU, functional checks only): render() brackets its
+    launches with host synchronize + barrier (the same barriers on every
+    rank), so each device wait finds its flags already raised and no kernel
+    ever spins on another process's kernel on the same GPU.
     """
 
-    def __init__(self, height: int, width: int, device: int, group=None, ipc=None):
+    SLOTS = _native.MAX_PEERS
+
+    def __init__(self, height: int, width: int, device: int, group=None, ipc=None, dest: int | None = None,
+                 host_ordered: bool = False, timeout_us: int = 20_000_000):
         import torch
         import torch.distributed as dist
 
@@ -180,43 +215,112 @@ class PeerFrames:
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        if self.world > self.SLOTS:
+            raise ValueError(f"at most {self.SLOTS} ranks")
+        if dest is not None and not 0 <= dest < self.world:
+            raise ValueError(f"dest must be a rank in [0, {self.world})")
+        self.dest = dest
+        self.receives = dest is None or dest == self.rank
+        self.host_ordered = host_ordered
+        self.timeout_us = int(timeout_us)
+        self.device = device
         self.ipc = ipc or _NativeIpc(device)
         self.nbytes = height * width * 4
-        self.frame_ptr = self.ipc.alloc(self.nbytes)
+        self.frame_alloc = -(-self.nbytes // 256) * 256
+        flag_bytes = 4 * self.SLOTS
+        total = self.frame_alloc + 2 * flag_bytes
+        self.base = self.ipc.alloc(total)
+        self.frame_ptr = self.base
+        on_device = isinstance(self.ipc, _NativeIpc)
+        if on_device:  # flags start at 0: nothing done, nothing released
+            torch.as_tensor(_DeviceBytes(self.base + self.frame_alloc, 2 * flag_bytes), device=f"cuda:{device}").zero_()
+            torch.cuda.synchronize(device)
         handles = [None] * self.world
-        dist.all_gather_object(handles, self.ipc.handle(self.frame_ptr), group=group)
+        dist.all_gather_object(handles, self.ipc.handle(self.base), group=group)
         self._opened = []
-        ptrs = []
+        bases = []
         for r, h in enumerate(handles):
             if r == self.rank:
-                ptrs.append(self.frame_ptr)
+                bases.append(self.base)
             else:
-                p = self.ipc.open(h)
-                self._opened.append(p)
-                ptrs.append(p)
-        self.peer_ptrs = ptrs
-        self.table = torch.tensor(ptrs, dtype=torch.int64,
-                                  device=f"cuda:{device}" if isinstance(self.ipc, _NativeIpc) else "cpu")
+                q = self.ipc.open(h)
+                self._opened.append(q)
+                bases.append(q)
+        self.peer_ptrs = bases
+        tdev = f"cuda:{device}" if on_device else "cpu"
+        self.table = torch.tensor(bases, dtype=torch.int64, device=tdev)
+        self.done_table = torch.tensor([b + self.frame_alloc for b in bases], dtype=torch.int64, device=tdev)
+        self.free_table = torch.tensor([b + self.frame_alloc + flag_bytes for b in bases], dtype=torch.int64,
+                                       device=tdev)
+        self.done_block = self.base + self.frame_alloc
+        self.free_block = self.done_block + flag_bytes
+        self.status = torch.zeros(2, dtype=torch.int32, device=tdev)
+        self.seq = 0
+        dist.barrier(group=group)  # every rank's flags are zeroed before anyone signals
+
+    # ---- per frame (stream-ordered, no host synchronisation)
+
+    def _host_order(self, stream_ptr: int) -> None:
+        if self.host_ordered:
+            import torch
+            import torch.distributed as dist
+
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group=self.group)
 
     def render(self, dv, P, counters_ptr: int, stream_ptr: int) -> None:
-        # the kernels store at image_row * width + px into every rank's
+        # the kernels store at image_row * width + px into every receiver's
         # mapped buffer: a frame of another size would write out of bounds
         if (int(P.height), int(P.width)) != (self.height, self.width):
             raise ValueError(f"frame {P.height}x{P.width} does not match the peer buffers "
                              f"{self.height}x{self.width}")
-        _native.check(_native.load().vc_render_to_peers(
-            dv.handle, ctypes.byref(P), ctypes.c_void_p(self.table.data_ptr()), self.world, self.nbytes,
-            ctypes.c_void_p(counters_ptr), ctypes.c_void_p(stream_ptr)))
+        L = _native.load()
+        self.seq += 1
+        if self.seq > 1:  # every receiver has read the previous frame out of this buffer pair
+            self._host_order(stream_ptr)
+            first, count = (0, self.world) if self.dest is None else (self.dest, 1)
+            _native.check(L.vc_wait_flags(ctypes.c_void_p(self.free_block), first, count, self.seq - 1,
+                                          self.timeout_us, ctypes.c_void_p(self.status.data_ptr()),
+                                          ctypes.c_void_p(stream_ptr)))
+        desc = _native.PeerFramesDesc(self.table.data_ptr(), self.done_table.data_ptr(), self.frame_alloc,
+                                      self.world, self.rank, -1 if self.dest is None else self.dest, self.seq)
+        _native.check(L.vc_render_to_peers(dv.handle, ctypes.byref(P), ctypes.byref(desc),
+                                           ctypes.c_void_p(counters_ptr), ctypes.c_void_p(stream_ptr)))
+        # host-ordered: every rank's bands and "done" flags are in place
+        # before any receiver's wait is launched (same barriers on all ranks)
+        self._host_order(stream_ptr)
+
+    def wait_frame(self, stream_ptr: int) -> None:
+        """Receiver: the stream waits until every rank's bands of frame
+        `seq` are in this rank's frame buffer."""
+        if not self.receives:
+            raise RuntimeError("this rank does not receive the frame (dest)")
+        _native.check(_native.load().vc_wait_flags(ctypes.c_void_p(self.done_block), 0, self.world, self.seq,
+                                                   self.timeout_us, ctypes.c_void_p(self.status.data_ptr() + 4),
+                                                   ctypes.c_void_p(stream_ptr)))
+
+    def release(self, stream_ptr: int) -> None:
+        """Receiver, after its reads of frame `seq` (stream-ordered): the
+        senders may overwrite this frame buffer."""
+        _native.check(_native.load().vc_signal_flags(ctypes.c_void_p(self.free_table.data_ptr()), self.world, -1,
+                                                     self.rank, self.seq, ctypes.c_void_p(stream_ptr)))
+
+    def check(self) -> None:
+        """Raise if a device wait timed out (reads the status; synchronises)."""
+        st = self.status.cpu().tolist()
+        if any(st):
+            raise RuntimeError(f"peer flag wait timed out after {self.timeout_us} us (status {st})")
 
     def download(self, out: np.ndarray, stream_ptr: int = 0) -> np.ndarray:
         _native.check(_native.load().vc_memcpy_to_host(out.ctypes.data, ctypes.c_void_p(self.frame_ptr),
                                                        self.nbytes, ctypes.c_void_p(stream_ptr)))
+        self.check()
         return out
 
     def close(self) -> None:
         for p in self._opened:
             self.ipc.close(p)
         self._opened = []
-        if self.frame_ptr:
-            self.ipc.free(self.frame_ptr)
-            self.frame_ptr = 0
+        if self.base:
+            self.ipc.free(self.base)
+            self.base = self.frame_ptr = 0

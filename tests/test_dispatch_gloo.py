@@ -136,3 +136,77 @@ def test_gloo_peer_frame_handle_exchange():
         assert ptrs[rank] == 1000 + rank
         assert [p for r, p in enumerate(ptrs) if r != rank] == [1000 + r + 10_000 for r in range(world) if r != rank]
         assert opened == sorted(f"rank{r}:{1000 + r}" for r in range(world) if r != rank)
+
+
+class FakeNative:
+    """Records the flag-protocol calls PeerFrames makes (no device)."""
+
+    def __init__(self, log):
+        self.log = log
+
+    def vc_wait_flags(self, block, first, count, seq, timeout_us, status, stream):
+        self.log.append(("wait", block.value, first, count, seq))
+        return 0
+
+    def vc_signal_flags(self, table, n, dest, slot, seq, stream):
+        self.log.append(("signal", n, dest, slot, seq))
+        return 0
+
+    def vc_render_to_peers(self, handle, P, desc, counters, stream):
+        d = desc._obj
+        self.log.append(("render", d.n, d.self, d.dest, d.seq))
+        return 0
+
+
+def _protocol_worker(rank, world, port, dest, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1609_01317_b200 import _native, dispatch
+
+        log = []
+        _native.load = lambda *a, **k: FakeNative(log)
+        pf = dispatch.PeerFrames(36, 20, device=0, ipc=FakeIpc(rank), dest=dest)
+
+        P = _native.RenderParams()
+        P.height, P.width = 36, 20
+
+        for _ in range(3):
+            pf.render(type("DV", (), {"handle": None})(), P, 0, 0)
+            if pf.receives:
+                pf.wait_frame(0)
+                pf.release(0)
+        q.put((rank, pf.done_block, pf.free_block, log))
+        pf.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dest", [None, 0])
+def test_gloo_peer_flag_protocol(dest):
+    """Per frame, with no host barrier: a sender waits for the receivers'
+    'free' flags of the previous use (from the second frame on), renders with
+    the frame's sequence number; a receiver waits for every rank's 'done'
+    flag and then releases its slot in every sender's 'free' block."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_protocol_worker, args=(r, world, port, dest, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, done_block, free_block, log in sorted(q.get(timeout=5) for _ in range(world)):
+        receives = dest is None or dest == rank
+        first, count = (0, world) if dest is None else (dest, 1)
+        want = []
+        for seq in (1, 2, 3):
+            if seq > 1:
+                want.append(("wait", free_block, first, count, seq - 1))
+            want.append(("render", world, rank, -1 if dest is None else dest, seq))
+            if receives:
+                want.append(("wait", done_block, 0, world, seq))
+                want.append(("signal", world, -1, rank, seq))
+        assert log == want, (rank, log)

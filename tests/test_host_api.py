@@ -32,7 +32,7 @@ def test_library_exports_every_header_symbol():
     assert set(syms) == set(_native.EXPORTS)
     for s in syms:
         assert hasattr(L, s), s
-    assert L.vc_abi_version() == 3
+    assert L.vc_abi_version() == 4
     assert L.vc_render_params_size() == ctypes.sizeof(_native.RenderParams)
 
 

@@ -1,12 +1,17 @@
 """The fused peer-store gather across real processes (one GPU).
 
-Two or three ranks (gloo process group for the handle exchange and the barrier --
-no NCCL, no kernel waits on another rank) each allocate a full frame with
-vc_device_alloc, exchange CUDA IPC handles, map each other's frame and run
-vc_render_to_peers on their own interleaved bands.  After both kernels and
-one barrier, each rank's frame must equal the single-process render_frame.
-This exercises the real IPC mapping and the cross-process stores of the
-multi-GPU path; only the NVLink hop is absent.
+Two or three ranks (gloo process group for the handle exchange) each
+allocate a frame + flag blocks with vc_device_alloc, exchange CUDA IPC
+handles, map each other's allocation and run PeerFrames.render on their own
+interleaved bands: tile pushes into the receivers' frames and a
+system-scope release of their "done" flags; receivers wait on the flags,
+download, and release the buffers through the senders' "free" flags; two
+frames go through the same buffers.  All ranks share the one GPU, so the
+waits are host-ordered (PeerFrames(host_ordered=True)): each device wait is
+preceded by a host barrier and never spins on another process's kernel.
+Each receiver's frames must equal the single-process render_frame.  This
+exercises the real IPC mapping, the cross-process stores and flag
+visibility of the multi-GPU path; only the NVLink hop is absent.
 """
 
 from __future__ import annotations
@@ -34,19 +39,28 @@ WORKER = textwrap.dedent("""
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
+    dest = None if sys.argv[3] == "all" else int(sys.argv[3])
     vol = phantoms.ct_phantom(96)
-    sc, st = phantoms.scene_c3(vol, width=200, height=120, azimuth=20.0)
     dv = vc.device_volume(vol)
-    pf = PeerFrames(st.height, st.width, 0)
+    sc, st = phantoms.scene_c3(vol, width=200, height=120, azimuth=20.0)
+    # host_ordered: every process shares the one GPU, so no device wait may
+    # spin on another process's kernel -- a host barrier precedes each wait
+    pf = PeerFrames(st.height, st.width, 0, dest=dest, host_ordered=True)
     plan = BandPlan(st.height, st.width, band_rows=8, world=world, rank=rank)
-    P = render_params(vol, sc, st, band_rows=plan.band_rows, band_first=rank, band_step=world)
-    pf.render(dv, P, 0, 0)
+    stream = torch.cuda.current_stream().cuda_stream
+    for f, az in enumerate((20.0, 140.0)):  # two frames through the same buffers: the "free" flags
+        sc, st = phantoms.scene_c3(vol, width=200, height=120, azimuth=az)
+        P = render_params(vol, sc, st, band_rows=plan.band_rows, band_first=rank, band_step=world)
+        pf.render(dv, P, 0, stream)
+        if pf.receives:
+            pf.wait_frame(stream)
+            img = pf.download(np.empty((st.height, st.width, 4), np.uint8), stream)
+            pf.release(stream)
+            np.save(sys.argv[2] + f"_f{f}_rank{rank}.npy", img)
+        if rank == 0:
+            np.save(sys.argv[2] + f"_f{f}_ref.npy", vc.render_frame(vol, sc, st).pixels)
     torch.cuda.synchronize()
-    dist.barrier()
-    img = pf.download(np.empty((st.height, st.width, 4), np.uint8))
-    np.save(sys.argv[2] + f"_rank{rank}.npy", img)
-    if rank == 0:
-        np.save(sys.argv[2] + "_ref.npy", vc.render_frame(vol, sc, st).pixels)
+    pf.check()
     dist.barrier()
     pf.close()
     dist.destroy_process_group()
@@ -60,8 +74,8 @@ def _free_port() -> int:
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 3])
-def test_peer_store_gather_across_processes(tmp_path, world):
+@pytest.mark.parametrize("world,dest", [(2, "all"), (3, "all"), (3, "0")])
+def test_peer_store_gather_across_processes(tmp_path, world, dest):
     script = tmp_path / "worker.py"
     script.write_text(WORKER)
     out = str(tmp_path / "frame")
@@ -69,7 +83,7 @@ def test_peer_store_gather_across_processes(tmp_path, world):
     procs = []
     for r in range(world):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1", MASTER_PORT=port)
-        procs.append(subprocess.Popen([sys.executable, str(script), str(ROOT), out], env=env,
+        procs.append(subprocess.Popen([sys.executable, str(script), str(ROOT), out, dest], env=env,
                                       stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
     logs = []
     for p in procs:
@@ -80,10 +94,12 @@ def test_peer_store_gather_across_processes(tmp_path, world):
             o, _ = p.communicate()
         logs.append(o)
         assert p.returncode == 0, o[-3000:]
-    ref = np.load(out + "_ref.npy")
-    for r in range(world):
-        got = np.load(out + f"_rank{r}.npy")
-        assert np.array_equal(got, ref), f"rank {r} frame differs"
+    receivers = range(world) if dest == "all" else [int(dest)]
+    for f in range(2):
+        ref = np.load(out + f"_f{f}_ref.npy")
+        for r in receivers:
+            got = np.load(out + f"_f{f}_rank{r}.npy")
+            assert np.array_equal(got, ref), f"frame {f}: rank {r} differs"
 
 
 @pytest.mark.gpu

@@ -70,14 +70,21 @@ def main():
                                     transfer=s2.transfer), replace(t2, gradient_source="volume"))
     fb = vc.render_frame(ct, sc, st)
     vc.png_bytes(fb.pixels)
-    # vc_render_to_peers with a one-entry table of local frames
-    frame = torch.zeros((st.height, st.width, 4), dtype=torch.uint8, device="cuda")
-    table = torch.tensor([frame.data_ptr()], dtype=torch.int64, device="cuda")
-    P = render_params(ct, sc, st)
-    _native.check(L.vc_render_to_peers(vc.device_volume(ct).handle, ctypes.byref(P),
-                                       ctypes.c_void_p(table.data_ptr()), 1, frame.numel(), None, None))
-    torch.cuda.synchronize()
-    assert np.array_equal(frame.cpu().numpy(), fb.pixels)
+    # vc_render_to_peers: two virtual ranks in one process (tile pushes with
+    # band_rows 8, per-pixel stores with band_rows 6) + done flags
+    frames = [torch.zeros((st.height, st.width, 4), dtype=torch.uint8, device="cuda") for _ in range(2)]
+    done = [torch.zeros(_native.MAX_PEERS, dtype=torch.int32, device="cuda") for _ in range(2)]
+    ftab = torch.tensor([f.data_ptr() for f in frames], dtype=torch.int64, device="cuda")
+    dtab = torch.tensor([d.data_ptr() for d in done], dtype=torch.int64, device="cuda")
+    for seq, band_rows in ((1, 8), (2, 6)):
+        for r in range(2):
+            P = render_params(ct, sc, st, band_rows=band_rows, band_first=r, band_step=2)
+            desc = _native.PeerFramesDesc(ftab.data_ptr(), dtab.data_ptr(), frames[0].numel(), 2, r, -1, seq)
+            _native.check(L.vc_render_to_peers(vc.device_volume(ct).handle, ctypes.byref(P), ctypes.byref(desc),
+                                               None, None))
+        torch.cuda.synchronize()
+        for f in frames:
+            assert np.array_equal(f.cpu().numpy(), fb.pixels)
     if a.out:
         np.savez_compressed(a.out, **saved)
     report = {"scenes": "ok", "library": str(_native.library_path())}
