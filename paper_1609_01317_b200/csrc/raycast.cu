@@ -93,7 +93,10 @@ __device__ __forceinline__ double ceil_pos(double x) {
 // inside the real box after the reference's rounding (error ~1e-13 voxel):
 // they read provably out-of-window values and are skipped.  Only this
 // conservativeness matters here, not bit-exactness.
-__device__ __forceinline__ double skip_to(double t, double k, double base, const Skip& sk,
+// LAZY (shade stage, few skip events per ray): the reciprocal speeds are
+// recomputed here from the direction instead of living in registers
+template <bool LAZY = false>
+__device__ __forceinline__ double skip_to(double t, double k, double base, const Skip& sk, const RayPos& rp,
                                           const double p[3], const int c[3], int d) {
     constexpr double EPS = 1e-6;
     const int r = (d - 1) << MC_SHIFT;
@@ -101,7 +104,7 @@ __device__ __forceinline__ double skip_to(double t, double k, double base, const
 #pragma unroll
     for (int a = 0; a < 3; a++) {
         const int lo = (c[a] >> MC_SHIFT) << MC_SHIFT;
-        const double ib = sk.ib[a];
+        const double ib = LAZY ? (rp.d[a] == 0.0 ? 0.0 : dmul(rp.s[a], __drcp_rn(rp.d[a]))) : sk.ib[a];
         // the box face ahead, in voxel units (branch-free: selects, one exact
         // int -> double on the FP64 pipe); a zero direction adds no limit
         const bool up = ib > 0.0;
@@ -139,7 +142,7 @@ __device__ __forceinline__ bool tex_in_window(const TexArgs& t, const double p[3
 // One lattice sample of the march: -1 when empty-space skipping proves it
 // out of window (k has been advanced, no fetch), else whether the
 // reference's sample_any at p lies in the threshold window (0 / 1).
-template <typename T, int INTERP>
+template <typename T, int INTERP, bool LAZY = false>
 __device__ __forceinline__ int march_sample(const Ctx<T>& C, const vc_render_params& P, const double p[3],
                                             double t, double& k, double base, unsigned& nskip) {
     if (INTERP != VC_TRILINEAR && INTERP != VC_TEX) {
@@ -154,7 +157,7 @@ __device__ __forceinline__ int march_sample(const Ctx<T>& C, const vc_render_par
             const int d = vc_ldg(C.sk.dist + macro_index(C.sk, L));
             if (d != 0) {
                 const int c[3] = {L.i, L.j, L.k};
-                const double kn = skip_to(t, k, base, C.sk, p, c, d);
+                const double kn = skip_to<LAZY>(t, k, base, C.sk, C.rp, p, c, d);
                 nskip += 1;
                 k = kn;
                 return -1;
@@ -173,7 +176,7 @@ __device__ __forceinline__ int march_sample(const Ctx<T>& C, const vc_render_par
         const int d = vc_ldg(C.sk.dist + macro_index(C.sk, L));
         if (d != 0) {
             const int c[3] = {L.i, L.j, L.k};
-            const double kn = skip_to(t, k, base, C.sk, p, c, d);
+            const double kn = skip_to<LAZY>(t, k, base, C.sk, C.rp, p, c, d);
             nskip += 1;  // one empty-space jump (counting the samples it skips costs 3%)
             k = kn;
             return -1;
@@ -327,6 +330,33 @@ __device__ __noinline__ double4 grad_taps(Vol<T> v, double x, double y, double z
     return make_double4(g[0], g[1], g[2], __longlong_as_double(0x7ff8000000000000LL));
 }
 
+// _shade_sample's value and diffuse term from the reference taps
+// (_kernels.py:549-571): (illum before clamping, value)
+template <typename T, int OP, int SI>
+__device__ __forceinline__ double2 taps_illum_value_inl(const Vol<T>& v, double p0, double p1, double p2, double wx,
+                                                        double wy, double wz, double lpx, double lpy, double lpz) {
+    const double4 gg = grad_taps<T, OP>(v, p0, p1, p2);
+    double g[3] = {gg.x, gg.y, gg.z};
+    // the footprint's centre is sample_trilinear(p) (bit-identical)
+    const double val = (SI == VC_TRILINEAR && gg.w == gg.w) ? gg.w : sample_any<T, SI>(v, p0, p1, p2);
+    double u[3];
+    normalize3(g, u);
+    // field values rise toward the interior, the surface normal points away
+    const double snx = -u[0], sny = -u[1], snz = -u[2];
+    const double lx = dsub(lpx, wx);
+    const double ly = dsub(lpy, wy);
+    const double lz = dsub(lpz, wz);
+    const double ln = __dsqrt_rn(dadd(dadd(dmul(lx, lx), dmul(ly, ly)), dmul(lz, lz)));
+    double illum = 0.0;
+    if (ln > 0.0) illum = ddiv(dadd(dadd(dmul(lx, snx), dmul(ly, sny)), dmul(lz, snz)), ln);
+    return make_double2(illum, val);
+}
+template <typename T, int OP, int SI>
+__device__ __noinline__ double2 taps_illum_value(Vol<T> v, double p0, double p1, double p2, double wx, double wy,
+                                                 double wz, double lpx, double lpy, double lpz) {
+    return taps_illum_value_inl<T, OP, SI>(v, p0, p1, p2, wx, wy, wz, lpx, lpy, lpz);
+}
+
 // _kernels.py:528-579
 // GV: shading gradient from the packed volume (C.grad != nullptr) -- a
 // template parameter so the taps-only kernel carries none of that code
@@ -400,20 +430,18 @@ __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_pa
 #ifdef VC_DEBUG_TAPS
         if (GV) atomicAdd(&g_debug_taps, 1u);
 #endif
-        const double4 gg = grad_taps<T, OP>(C.v, p[0], p[1], p[2]);
-        double g[3] = {gg.x, gg.y, gg.z};
-        // the footprint's centre is sample_trilinear(p) (bit-identical)
         constexpr int SI = INTERP == VC_TEX ? VC_TRILINEAR : INTERP;  // boundary band: software value
-        val = (SI == VC_TRILINEAR && gg.w == gg.w) ? gg.w : sample_any<T, SI>(C.v, p[0], p[1], p[2]);
-        double u[3];
-        normalize3(g, u);
-        // field values rise toward the interior, the surface normal points away
-        const double snx = -u[0], sny = -u[1], snz = -u[2];
-        const double lx = dsub(P.light_pos[0], wx);
-        const double ly = dsub(P.light_pos[1], wy);
-        const double lz = dsub(P.light_pos[2], wz);
-        const double ln = __dsqrt_rn(dadd(dadd(dmul(lx, lx), dmul(ly, ly)), dmul(lz, lz)));
-        if (ln > 0.0) illum = ddiv(dadd(dadd(dmul(lx, snx), dmul(ly, sny)), dmul(lz, snz)), ln);
+        if constexpr (GV) {  // the rare path of the gradient-volume kernel: out of line
+            const double2 iv = taps_illum_value<T, OP, SI>(C.v, p[0], p[1], p[2], wx, wy, wz, P.light_pos[0],
+                                                           P.light_pos[1], P.light_pos[2]);
+            illum = iv.x;
+            val = iv.y;
+        } else {
+            const double2 iv = taps_illum_value_inl<T, OP, SI>(C.v, p[0], p[1], p[2], wx, wy, wz, P.light_pos[0],
+                                                               P.light_pos[1], P.light_pos[2]);
+            illum = iv.x;
+            val = iv.y;
+        }
     }
     illum = clamp01(illum);
     const double hu = dmul(div_rcp(dsub(val, P.mu_water), P.mu_water, C.rmu), 1000.0);
@@ -571,7 +599,7 @@ __device__ __noinline__ double adaptive_stride(const OctDev o, const StrideArgs 
 
 // One lattice step of the march base + k*coarse (first_hit's loop body,
 // _kernels.py:410-436 / the composite loop :756-765).
-template <typename T, int INTERP>
+template <typename T, int INTERP, bool LAZY = false>
 __device__ __forceinline__ void march_step(const Ctx<T>& C, const vc_render_params& P, RayState& R,
                                            unsigned& nsamp, unsigned& nskip, const OctDev* oct = nullptr) {
     const double t = dadd(R.base, dmul(R.k, P.coarse));
@@ -581,7 +609,7 @@ __device__ __forceinline__ void march_step(const Ctx<T>& C, const vc_render_para
     }
     double p[3];
     C.rp.at(t, p);
-    const int w = march_sample<T, INTERP>(C, P, p, t, R.k, R.base, nskip);
+    const int w = march_sample<T, INTERP, LAZY>(C, P, p, t, R.k, R.base, nskip);
     if (w < 0) return;
     nsamp++;
     if (oct != nullptr && !w) {  // first-hit stage, adaptive mode
@@ -790,12 +818,6 @@ struct __align__(16) HitEntry {
 };
 static_assert(sizeof(HitEntry) == 48, "hit queue entry layout");
 __device__ __forceinline__ uint32_t pack_pix(int lr, int px) { return ((uint32_t)lr << 16) | (uint32_t)px; }
-
-// the skip reciprocals start_ray computes, from a queued direction
-__device__ __forceinline__ void skip_rcp(const RayPos& rp, Skip& sk) {
-#pragma unroll
-    for (int a = 0; a < 3; a++) sk.ib[a] = rp.d[a] == 0.0 ? 0.0 : dmul(rp.s[a], __drcp_rn(rp.d[a]));
-}
 
 // Work counters of one launch pair (zeroed together before the frame).
 struct FrameWork {
@@ -1309,7 +1331,6 @@ __global__ void __launch_bounds__(128, GV ? VC_SHV_MINB : VC_SH_MINB) shade_kern
                     lr = (int)(e.pix >> 16);
 #pragma unroll
                     for (int a = 0; a < 3; a++) C.rp.d[a] = e.d[a];
-                    skip_rcp(C.rp, C.sk);
                     R.lim = e.lim;
                     R.base = e.t_star;
                     R.k = 1.0;
@@ -1329,7 +1350,7 @@ __global__ void __launch_bounds__(128, GV ? VC_SHV_MINB : VC_SH_MINB) shade_kern
             if (mneed == 0) break;
             const unsigned mact = __ballot_sync(FULL, active);
             if (__popc(mact & ~mneed) * READY_DEN >= __popc(mact) * (GV ? VC_SHV_READY : VC_SH_READY)) break;
-            if (need) march_step<T, INTERP>(C, P, R, nsamp, nskip);
+            if (need) march_step<T, INTERP, true>(C, P, R, nsamp, nskip);
         }
         if (active && (R.found || R.exhausted)) {
             uchar4 o;
