@@ -72,6 +72,17 @@ def _scene(rng, arr, name):
     return vol, sc, st
 
 
+def zero_window_scene(rng, vol, sc):
+    """The scene with a threshold window containing 0 (lower bound 0 or below):
+    with use_octree the reference skips in-window border samples through its
+    octree segments, which the device replays."""
+    vmax = float(vol.as_array().max())
+    lo = -float(rng.uniform(0.0, 0.3)) * vmax if rng.random() < 0.7 else 0.0
+    hi = float(rng.uniform(0.02, 0.7)) * vmax
+    return vc.Scene(camera=sc.camera, light=sc.light, window=vc.ThresholdWindow(lo, hi),
+                    transfer=sc.transfer, clip=sc.clip)
+
+
 @pytest.fixture(scope="module")
 def volumes():
     return _volumes()
@@ -127,3 +138,23 @@ def test_gradient_volume_cancellation_regression(volumes):
     want, _ = oracle.render(vol.as_array(), vol.spacing, spec_of((sc, st)), threads=8)
     fb = vc.render_frame(vol, sc, replace(st, gradient_source="volume"))
     assert int(np.abs(fb.pixels.astype(int) - want.astype(int)).max()) <= 1
+
+
+@pytest.mark.parametrize("i", range(24))
+def test_random_zero_window_scene_vs_oracle(volumes, i):
+    """0 inside the window: use_octree=False is the brute-force march,
+    use_octree=True the reference's octree-segment walk (oracle octree=True,
+    pinned to the reference's zerowin goldens) -- pixels and counts."""
+    rng = np.random.default_rng(9000 + i)
+    name = ["ct", "noise", "ml"][i % 3]
+    vol, sc, st = _scene(rng, volumes[name], name)
+    sc = zero_window_scene(rng, vol, sc)
+    for oct_on in (False, True):
+        st2 = replace(st, use_octree=oct_on)
+        want, want_count = oracle.render(vol.as_array(), vol.spacing, spec_of((sc, st2)), threads=8, octree=True)
+        fb = vc.render_frame(vol, sc, st2)
+        d = np.abs(fb.pixels.astype(int) - want.astype(int))
+        assert d.max() == 0, (oct_on, int((d > 0).any(axis=2).sum()), int(d.max()))
+        assert fb.sample_count == want_count, oct_on
+        fb = vc.render_frame(vol, sc, replace(st2, gradient_source="volume"))
+        assert int(np.abs(fb.pixels.astype(int) - want.astype(int)).max()) <= 1

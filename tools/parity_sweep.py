@@ -22,7 +22,7 @@ import numpy as np  # noqa: E402
 import paper_1609_01317_b200 as vc  # noqa: E402
 from oracle import oracle  # noqa: E402
 from tests.specs import spec_of  # noqa: E402
-from tests.test_gpu_random import _scene, _volumes  # noqa: E402
+from tests.test_gpu_random import _scene, _volumes, zero_window_scene  # noqa: E402
 
 
 def main():
@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--scenes", type=int, default=1000)
     ap.add_argument("--adaptive", type=int, default=300)
     ap.add_argument("--first-seed", type=int, default=100000)
+    ap.add_argument("--zero-window", type=int, default=0,
+                    help="scenes with 0 inside the threshold window (use_octree replays the octree walk)")
     ap.add_argument("--big", action="store_true",
                     help="128^3 CT / 96^3 Marschner-Lobb / 48x40x56 noise volumes and 3x the image size")
     a = ap.parse_args()
@@ -45,7 +47,7 @@ def main():
     res = {"scenes": 0, "brute_force_pixel_mismatch": 0, "count_mismatch": 0, "skipping_pixel_mismatch": 0,
            "gradient_volume_over_1lsb": 0, "gradient_volume_max_lsb": 0,
            "adaptive_scenes": 0, "adaptive_pixel_mismatch": 0, "adaptive_count_mismatch": 0,
-           "adaptive_octree_scenes": 0, "failures": []}
+           "adaptive_octree_scenes": 0, "zero_window_scenes": 0, "zero_window_mismatch": 0, "failures": []}
     t0 = time.perf_counter()
     for n in range(a.scenes):
         seed = a.first_seed + n
@@ -91,6 +93,26 @@ def main():
         if fb.sample_count != cnt:
             res["adaptive_count_mismatch"] += 1
             res["failures"].append(("adaptive_count", seed))
+    for n in range(a.zero_window):
+        seed = a.first_seed + 900000 + n
+        rng = np.random.default_rng(seed)
+        vol, sc, st = _scene(rng, vols[names[n % 3]], names[n % 3])
+        if a.big:
+            st = replace(st, width=3 * st.width, height=3 * st.height)
+        sc = zero_window_scene(rng, vol, sc)
+        res["zero_window_scenes"] += 1
+        for oct_on in (False, True):
+            st2 = replace(st, use_octree=oct_on)
+            want, cnt = oracle.render(vol.as_array(), vol.spacing, spec_of((sc, st2)), octree=True)
+            fb = vc.render_frame(vol, sc, st2)
+            if not np.array_equal(fb.pixels, want) or fb.sample_count != cnt:
+                res["zero_window_mismatch"] += 1
+                res["failures"].append(("zero_window", seed, oct_on))
+            d = int(np.abs(vc.render_frame(vol, sc, replace(st2, gradient_source="volume")).pixels.astype(int)
+                           - want.astype(int)).max())
+            if d > 1:
+                res["gradient_volume_over_1lsb"] += 1
+                res["failures"].append(("zero_window_gv", seed, oct_on, d))
     res["seconds"] = round(time.perf_counter() - t0, 1)
     res["failures"] = res["failures"][:50]
     print(json.dumps(res))
