@@ -429,10 +429,8 @@ __device__ __forceinline__ float vox_f32(wide_t<T> c) {
 }
 
 template <typename T>
-__device__ __forceinline__ bool in_window_trilinear(const Vol<T>& v, const Loc& L, double t_low, double t_high,
-                                                    const WinF& w) {
-    wide_t<T> c[8];  // L is clamped: i+1 < n unless n == 1
-    gather8(v, L.i, L.j, L.k, c);
+__device__ __forceinline__ bool in_window_corners(const wide_t<T> c[8], const Loc& L, double t_low, double t_high,
+                                                  const WinF& w) {
     const wide_t<T> c000 = c[0], c100 = c[1], c010 = c[2], c110 = c[3], c001 = c[4], c101 = c[5], c011 = c[6],
                     c111 = c[7];
     const float fx = __double2float_rn(L.fx), fy = __double2float_rn(L.fy), fz = __double2float_rn(L.fz);
@@ -449,6 +447,14 @@ __device__ __forceinline__ bool in_window_trilinear(const Vol<T>& v, const Loc& 
     const double x11 = lerp_vox<T>(c011, c111, L.fx);
     const double val = lerp(lerp(x00, x10, L.fy), lerp(x01, x11, L.fy), L.fz);
     return t_low <= val && val <= t_high;
+}
+
+template <typename T>
+__device__ __forceinline__ bool in_window_trilinear(const Vol<T>& v, const Loc& L, double t_low, double t_high,
+                                                    const WinF& w) {
+    wide_t<T> c[8];  // L is clamped: i+1 < n unless n == 1
+    gather8(v, L.i, L.j, L.k, c);
+    return in_window_corners<T>(c, L, t_low, t_high, w);
 }
 
 // _kernels.py:67-72
