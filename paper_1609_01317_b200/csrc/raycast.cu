@@ -714,7 +714,10 @@ __device__ __forceinline__ bool shade_and_composite(const Ctx<T>& C, const vc_re
 #define VC_FH_READY 4
 #endif
 #ifndef VC_SH_READY
-#define VC_SH_READY 2
+#define VC_SH_READY 1
+#endif
+#ifndef VC_SH_REFILL  // shade stage: idle lanes before a refill
+#define VC_SH_REFILL 24
 #endif
 #ifndef VC_SHV_READY  // shade stage, gradient-volume kernel
 #define VC_SHV_READY 1
@@ -1318,9 +1321,13 @@ __global__ void __launch_bounds__(128, GV ? VC_SHV_MINB : VC_SH_MINB) shade_kern
     for (;;) {
         // refill: a fresh lane starts "found" at its t_star, so its first
         // shade joins the other lanes' shades in the single resolve step below
+        // (only once VC_SH_REFILL lanes are idle, or none is active: each
+        // refill stalls the warp on the queue reads)
         for (;;) {
             const bool want = !active && !done;
-            if (__ballot_sync(FULL, want) == 0) break;
+            const unsigned mw = __ballot_sync(FULL, want);
+            if (mw == 0) break;
+            if (__popc(mw) < VC_SH_REFILL && __ballot_sync(FULL, active) != 0) break;
             const unsigned q = warp_ticket(&work->shades, want);
             if (want) {
                 if (q >= total) {
