@@ -711,18 +711,18 @@ __device__ __forceinline__ bool shade_and_composite(const Ctx<T>& C, const vc_re
 // a warp leaves the march loop when READY_NUM / READY_DEN of its live lanes
 // have a hit (or an exhausted ray) to resolve (first-hit / shade kernel)
 #ifndef VC_FH_READY
-#define VC_FH_READY 4
+#define VC_FH_READY 32
 #endif
 #ifndef VC_SH_READY
-#define VC_SH_READY 1
+#define VC_SH_READY 8
 #endif
 #ifndef VC_SH_REFILL  // shade stage: idle lanes before a refill
 #define VC_SH_REFILL 24
 #endif
 #ifndef VC_SHV_READY  // shade stage, gradient-volume kernel
-#define VC_SHV_READY 1
+#define VC_SHV_READY 8
 #endif
-constexpr int READY_DEN = 4;
+constexpr int READY_DEN = 32;
 
 // Where finished pixels go: the packed local rows of this rank (npeers == 0)
 // or, fused with the image-tile gather, the full frame buffers of the ranks
