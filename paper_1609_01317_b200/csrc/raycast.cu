@@ -322,20 +322,20 @@ struct Rgba {
 // showed instruction-cache stalls).
 // .w of the result: sample_trilinear at the point when the shared-footprint
 // path applied (NaN otherwise)
-template <typename T, int OP>
+template <typename T, int OP, bool ROLL = false>
 __device__ __noinline__ double4 grad_taps(Vol<T> v, double x, double y, double z) {
     double g[3], center;
     if (grad_raw_shared<T, OP>(v, x, y, z, g, center)) return make_double4(g[0], g[1], g[2], center);
-    grad_raw<T, OP>(v, x, y, z, g);
+    grad_raw<T, OP, ROLL>(v, x, y, z, g);
     return make_double4(g[0], g[1], g[2], __longlong_as_double(0x7ff8000000000000LL));
 }
 
 // _shade_sample's value and diffuse term from the reference taps
 // (_kernels.py:549-571): (illum before clamping, value)
-template <typename T, int OP, int SI>
+template <typename T, int OP, int SI, bool ROLL>
 __device__ __forceinline__ double2 taps_illum_value_inl(const Vol<T>& v, double p0, double p1, double p2, double wx,
                                                         double wy, double wz, double lpx, double lpy, double lpz) {
-    const double4 gg = grad_taps<T, OP>(v, p0, p1, p2);
+    const double4 gg = grad_taps<T, OP, ROLL>(v, p0, p1, p2);
     double g[3] = {gg.x, gg.y, gg.z};
     // the footprint's centre is sample_trilinear(p) (bit-identical)
     const double val = (SI == VC_TRILINEAR && gg.w == gg.w) ? gg.w : sample_any<T, SI>(v, p0, p1, p2);
@@ -351,10 +351,10 @@ __device__ __forceinline__ double2 taps_illum_value_inl(const Vol<T>& v, double 
     if (ln > 0.0) illum = ddiv(dadd(dadd(dmul(lx, snx), dmul(ly, sny)), dmul(lz, snz)), ln);
     return make_double2(illum, val);
 }
-template <typename T, int OP, int SI>
+template <typename T, int OP, int SI, bool ROLL>
 __device__ __noinline__ double2 taps_illum_value(Vol<T> v, double p0, double p1, double p2, double wx, double wy,
                                                  double wz, double lpx, double lpy, double lpz) {
-    return taps_illum_value_inl<T, OP, SI>(v, p0, p1, p2, wx, wy, wz, lpx, lpy, lpz);
+    return taps_illum_value_inl<T, OP, SI, ROLL>(v, p0, p1, p2, wx, wy, wz, lpx, lpy, lpz);
 }
 
 // _kernels.py:528-579
@@ -431,14 +431,17 @@ __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_pa
         if (GV) atomicAdd(&g_debug_taps, 1u);
 #endif
         constexpr int SI = INTERP == VC_TEX ? VC_TRILINEAR : INTERP;  // boundary band: software value
+        // the general taps loop rolled except in the integer-grid
+        // gradient-volume kernels (grad_raw: register pressure vs icache)
+        constexpr bool ROLL = !GV || !std::is_integral<T>::value;
         if constexpr (GV) {  // the rare path of the gradient-volume kernel: out of line
-            const double2 iv = taps_illum_value<T, OP, SI>(C.v, p[0], p[1], p[2], wx, wy, wz, P.light_pos[0],
-                                                           P.light_pos[1], P.light_pos[2]);
+            const double2 iv = taps_illum_value<T, OP, SI, ROLL>(C.v, p[0], p[1], p[2], wx, wy, wz, P.light_pos[0],
+                                                                 P.light_pos[1], P.light_pos[2]);
             illum = iv.x;
             val = iv.y;
         } else {
-            const double2 iv = taps_illum_value_inl<T, OP, SI>(C.v, p[0], p[1], p[2], wx, wy, wz, P.light_pos[0],
-                                                               P.light_pos[1], P.light_pos[2]);
+            const double2 iv = taps_illum_value_inl<T, OP, SI, ROLL>(C.v, p[0], p[1], p[2], wx, wy, wz,
+                                                                     P.light_pos[0], P.light_pos[1], P.light_pos[2]);
             illum = iv.x;
             val = iv.y;
         }

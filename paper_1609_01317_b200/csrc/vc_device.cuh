@@ -520,7 +520,35 @@ __host__ __device__ constexpr double zh_inv(int i, int j, int k) {
 // Terms whose weight is 0 add +0.0 to a sum that can never be -0.0 (it
 // starts at +0.0 and round-to-nearest never produces -0.0 from a sum
 // of non-(-0.0) operands), so they are dropped without changing a bit.
+// ROLL: the 26-tap loop is not unrolled.  This general path serves the
+// shading samples of the boundary band, where the shared footprint does not
+// apply; unrolled, its 26 inlined trilinear taps are ~4k instructions, and
+// where the band is frequent (noise / Marschner-Lobb faces, C4) they evicted
+// the march and shade loop from the instruction cache (50% of the C4 shade
+// stage's stalls "no instruction"; rolled: 4.48 -> 3.26 ms).  Where the band
+// is rare and the kernel tight on registers (C3's gradient-volume kernel)
+// the unrolled form keeps fewer spills.
 template <typename T, int OP>
+__device__ __forceinline__ void grad_tap_term(const Vol<T>& v, double x, double y, double z, int i, int j, int k,
+                                              double& gx, double& gy, double& gz) {
+    const double s = tap(v, dadd(x, (double)i), dadd(y, (double)j), dadd(z, (double)k));
+    double wx, wy, wz;
+    if (OP == VC_OP_SOBEL3D) {
+        wx = (double)i * smooth_weight(j, k);
+        wy = (double)j * smooth_weight(i, k);
+        wz = (double)k * smooth_weight(i, j);
+    } else {
+        const double inv = zh_inv(i, j, k);
+        wx = (double)i * inv;
+        wy = (double)j * inv;
+        wz = (double)k * inv;
+    }
+    if (i != 0) gx = dadd(gx, dmul(wx, s));
+    if (j != 0) gy = dadd(gy, dmul(wy, s));
+    if (k != 0) gz = dadd(gz, dmul(wz, s));
+}
+
+template <typename T, int OP, bool ROLL = false>
 __device__ __forceinline__ void grad_raw(const Vol<T>& v, double x, double y, double z, double g[3]) {
     if (OP == VC_OP_CENTRAL) {
         g[0] = dsub(tap(v, dadd(x, 1.0), y, z), tap(v, dsub(x, 1.0), y, z));
@@ -529,30 +557,22 @@ __device__ __forceinline__ void grad_raw(const Vol<T>& v, double x, double y, do
         return;
     }
     double gx = 0.0, gy = 0.0, gz = 0.0;
+    if constexpr (ROLL) {
+#pragma unroll 1
+        for (int i = -1; i < 2; i++)
+#pragma unroll 1
+            for (int j = -1; j < 2; j++)
+#pragma unroll 1
+                for (int k = -1; k < 2; k++)
+                    if (!(i == 0 && j == 0 && k == 0)) grad_tap_term<T, OP>(v, x, y, z, i, j, k, gx, gy, gz);
+    } else {
 #pragma unroll
-    for (int i = -1; i < 2; i++) {
+        for (int i = -1; i < 2; i++)
 #pragma unroll
-        for (int j = -1; j < 2; j++) {
+            for (int j = -1; j < 2; j++)
 #pragma unroll
-            for (int k = -1; k < 2; k++) {
-                if (i == 0 && j == 0 && k == 0) continue;
-                const double s = tap(v, dadd(x, (double)i), dadd(y, (double)j), dadd(z, (double)k));
-                double wx, wy, wz;
-                if (OP == VC_OP_SOBEL3D) {
-                    wx = (double)i * smooth_weight(j, k);
-                    wy = (double)j * smooth_weight(i, k);
-                    wz = (double)k * smooth_weight(i, j);
-                } else {
-                    const double inv = zh_inv(i, j, k);
-                    wx = (double)i * inv;
-                    wy = (double)j * inv;
-                    wz = (double)k * inv;
-                }
-                if (i != 0) gx = dadd(gx, dmul(wx, s));
-                if (j != 0) gy = dadd(gy, dmul(wy, s));
-                if (k != 0) gz = dadd(gz, dmul(wz, s));
-            }
-        }
+                for (int k = -1; k < 2; k++)
+                    if (!(i == 0 && j == 0 && k == 0)) grad_tap_term<T, OP>(v, x, y, z, i, j, k, gx, gy, gz);
     }
     g[0] = gx;
     g[1] = gy;
