@@ -54,6 +54,7 @@ struct Skip {
     int mx, my;        // macrocell grid dims (x, y)
     double ib[3];      // 1 / (ray direction in voxel units per unit t)
     double inv_coarse;
+    float inv_coarse_f;
     bool on;
     WinF win;          // float32 pre-test thresholds of the window
 };
@@ -680,6 +681,315 @@ __device__ __forceinline__ double refine_hit(const Ctx<T>& C, const vc_render_pa
     return tcur;
 }
 
+// ---- fixed-point lattice walk (first hit, trilinear) -----------------------
+// The reference forms every march position in float64 from scratch,
+// p(k) = (o + (base + k*coarse) * d) / s - 0.5, and only uses it to pick a
+// cell (floor), to test the cell's macrocell and to interpolate.  Here the
+// walk runs on p(k) = P0 + k*DP in 24.40 fixed point (two integer adds per
+// axis, no FP64 work) and is exact where it matters:
+//   * deviation.  |p_fx(k) - p_ref(k)| <= 2*Eref + (k+1)*2^-41 where Eref
+//     <= 2^-50 * ((|o| + 2T|d|) / s + |p| + 1) bounds the reference's own
+//     float64 rounding (T = |lim| + |base| + coarse).  fx_setup admits a
+//     ray only when Eref <= 2^-24, |p| <= 2^22 and k_last <= 2^19, so the
+//     deviation stays below 2^-21 (fine scan: + j*2^-41, j <= 2^18;
+//     bisection: each midpoint + 2^-41 + 2^-28, <= 64 of them): below
+//     0.75 * 2^-20 everywhere;
+//   * cells.  A coordinate whose fixed-point fraction lies within 2^-20 of
+//     a cell face ("guard") -- and every sample of a ray fx_setup did not
+//     admit -- takes the reference's float64 path; elsewhere floor(p_fx) ==
+//     floor(p_ref), so the range test, the macrocell and the eight gathered
+//     voxels are the reference's;
+//   * values.  The float32 pre-test uses the fixed-point fractions
+//     (truncated to 23 bits): error <= 2^-20 per fraction, <= 6 * amax *
+//     2^-20 = 96 * 2^-24 * amax over the three lerp levels; with the
+//     arithmetic's 34 * 2^-24 * amax that stays below the pre-test's E =
+//     256 * 2^-24 * amax.  An ambiguous value is re-evaluated with the
+//     reference's float64 position and cascade;
+//   * the end.  k > k_last <=> t(k) > lim: k_last is found once per ray
+//     with the march's own float64 t(k) (monotone in k);
+//   * skips.  Empty-space jumps only need conservativeness: the box-exit
+//     distance is formed in float32 from the cell, the fraction and a
+//     2^-8 voxel margin (float32 error <= 5e-4 voxel over a 1016-voxel box).
+constexpr double FX_ONE = 0x1p40;
+
+// Per-lane walk state.  It lives in shared memory (structure of arrays: a
+// warp's accesses are conflict-free) and is loaded into registers at the
+// top of each march phase; the march loop itself holds nothing else, so it
+// runs without spills, and the rare float64 fallbacks run between march
+// phases with the walk registers dead.  A ray fx_setup does not admit gets
+// p0 = dp = 0: its fractions are 0, inside the guard band, so every one of
+// its samples takes the float64 path.
+struct FxRay {
+    long long p0[3], dp[3];  // p(k) = p0 + k*dp, units of 2^-40 voxel
+    float ibf[3];            // s / d per axis (voxel -> t), 0 for d == 0
+    int klast;               // last lattice index with t(k) <= lim
+};
+
+struct FxLanes {
+    long long p0[3][128], dp[3][128];
+    float ibf[3][128];
+    int klast[128];
+    // direction and parameter bounds (fallbacks, refinement, hit entry)
+    double d[3][128], base[128], lim[128], t_enter[128];
+};
+
+__device__ __forceinline__ FxRay fx_load(const FxLanes& S, int me) {
+    FxRay F;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        F.p0[a] = S.p0[a][me];
+        F.dp[a] = S.dp[a][me];
+        F.ibf[a] = S.ibf[a][me];
+    }
+    F.klast = S.klast[me];
+    return F;
+}
+
+// the lane's RayPos (direction from the shared state)
+__device__ __forceinline__ RayPos fx_rp(const RayPos& rp0, const FxLanes& S, int me) {
+    RayPos rp = rp0;
+#pragma unroll
+    for (int a = 0; a < 3; a++) rp.d[a] = S.d[a][me];
+    return rp;
+}
+
+__device__ __forceinline__ long long to_fx(double v) { return __double2ll_rn(dmul(v, FX_ONE)); }
+
+__device__ __forceinline__ int fx_cell(long long x) { return (int)(x >> 40); }
+
+// p0 + k*dp for 0 <= k < 2^31 (two IMADs: unsigned wrap-around arithmetic)
+__device__ __forceinline__ long long fx_at(long long p0, long long dp, int k) {
+    return (long long)((unsigned long long)p0 + (unsigned long long)(unsigned)k * (unsigned long long)dp);
+}
+
+// fraction of a fixed-point coordinate, truncated to 23 bits; g |= within
+// 2^-20 of a cell face
+__device__ __forceinline__ float fx_frac(long long x, bool& g) {
+    const unsigned m = __funnelshift_l((unsigned)x, (unsigned)(x >> 32), 15);  // bits 39..17
+    const float F = __uint_as_float((m & 0x7fffffu) | 0x3f800000u);         // 1 + fraction
+    g = g || fabsf(__fsub_rn(F, 1.5f)) > 0.5f - 0x1p-20f;
+    return __fsub_rn(F, 1.0f);
+}
+
+template <typename T>
+__device__ __forceinline__ void fx_setup(const Ctx<T>& C, const vc_render_params& P, const RayState& R, FxLanes& S,
+                                         int me) {
+    bool ok = true;
+    double x = dmul(dsub(R.lim, R.base), C.sk.inv_coarse);
+    if (!(x < 524288.0)) {
+        ok = false;
+        x = 0.0;
+    }
+    int kl = (int)x;
+#pragma unroll 1
+    while (kl > 0 && dadd(R.base, dmul((double)kl, P.coarse)) > R.lim) kl--;
+#pragma unroll 1
+    while (kl < 524288 && dadd(R.base, dmul((double)(kl + 1), P.coarse)) <= R.lim) kl++;
+    S.klast[me] = kl;
+    double pb[3];
+    C.rp.at(R.base, pb);
+    const double tmax = fabs(R.lim) + fabs(R.base) + P.coarse;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        const double sl = dmul(dmul(P.coarse, C.rp.d[a]), C.rp.rs[a]);
+        const double e = (fabs(C.rp.o[a]) + 2.0 * tmax * fabs(C.rp.d[a])) * fabs(C.rp.rs[a]);
+        const double reach = fabs(pb[a]) + (double)(kl + 1) * fabs(sl);
+        ok = ok && e <= 0x1p24 && reach <= 0x1p22;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        S.p0[a][me] = ok ? to_fx(pb[a]) : 0;
+        S.dp[a][me] = ok ? to_fx(dmul(dmul(P.coarse, C.rp.d[a]), C.rp.rs[a])) : 0;
+        S.ibf[a][me] = C.rp.d[a] == 0.0 ? 0.0f : __double2float_rn(dmul(C.rp.s[a], __drcp_rn(C.rp.d[a])));
+        S.d[a][me] = C.rp.d[a];
+    }
+    S.base[me] = R.base;
+    S.lim[me] = R.lim;
+    S.t_enter[me] = R.t_enter;
+}
+
+__device__ __forceinline__ uint32_t macro_index3(const Skip& sk, int i, int j, int k) {
+    return ((uint32_t)(k >> MC_SHIFT) * (uint32_t)sk.my + (uint32_t)(j >> MC_SHIFT)) * (uint32_t)sk.mx +
+           (uint32_t)(i >> MC_SHIFT);
+}
+
+// skip_to for the fixed-point walk: float32 box-exit distance (see above)
+__device__ __forceinline__ int skip_fx(int k, const int c[3], const float f[3], const float ibf[3], float inv_coarse,
+                                       int d) {
+    constexpr float EPSF = 0x1p-8f;
+    const int r = (d - 1) << MC_SHIFT;
+    float dt = FLT_MAX;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        const int lo = (c[a] >> MC_SHIFT) << MC_SHIFT;
+        const bool up = ibf[a] > 0.0f;
+        const int rel = (up ? lo + (1 << MC_SHIFT) + r : lo - r) - c[a];  // face - cell, small
+        const float relf = __fsub_rn(__int_as_float(0x4b400000 + rel), 12582912.0f);
+        const float cand = __fmul_rn(__fsub_rn(__fadd_rn(relf, up ? -EPSF : EPSF), f[a]), ibf[a]);
+        dt = ibf[a] != 0.0f ? fminf(dt, cand) : dt;
+    }
+    int kn = k + 1;
+    if (dt > 0.0f) {
+        const float xs = __fmul_rn(dt, inv_coarse);
+        kn = xs < 0x1p30f ? max(kn, k + __float2int_ru(xs)) : 0x40000000;
+    }
+    return kn;
+}
+
+// One lattice step of the fixed-point walk at index k.  Returns false,
+// leaving k unchanged, when the sample needs the reference's float64 path
+// (a coordinate within 2^-20 of a cell face, or an ambiguous pre-test):
+// the lane then pauses until the warp's march phase ends (fx_exact_step).
+template <typename T>
+__device__ __forceinline__ bool march_step_fx(const Ctx<T>& C, const vc_render_params& P, RayState& R,
+                                              const FxRay& F, int& k, unsigned& nsamp, unsigned& nskip) {
+    if (k > F.klast) {
+        R.exhausted = true;
+        return true;
+    }
+    long long q[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) q[a] = fx_at(F.p0[a], F.dp[a], k);
+    bool g = false;
+    const int c[3] = {fx_cell(q[0]), fx_cell(q[1]), fx_cell(q[2])};
+    const float f[3] = {fx_frac(q[0], g), fx_frac(q[1], g), fx_frac(q[2], g)};
+    if (g) return false;
+    const bool inr = (unsigned)c[0] < (unsigned)(C.v.nx - 1) && (unsigned)c[1] < (unsigned)(C.v.ny - 1) &&
+                     (unsigned)c[2] < (unsigned)(C.v.nz - 1);
+    if (C.sk.on) {
+        if (!inr) {  // reads 0, outside the window when skipping is on
+            k++;
+            nskip++;
+            return true;
+        }
+        const int d = vc_ldg(C.sk.dist + macro_index3(C.sk, c[0], c[1], c[2]));
+        if (d != 0) {
+            k = skip_fx(k, c, f, F.ibf, C.sk.inv_coarse_f, d);
+            nskip++;
+            return true;
+        }
+    }
+    int w;
+    if (!inr) {
+        w = in_window(P, 0.0) ? 1 : 0;
+    } else {
+        w = window_cell_f<T>(C.v, c[0], c[1], c[2], f[0], f[1], f[2], C.sk.win);
+        if (w < 0) return false;
+    }
+    nsamp++;
+    k++;
+    if (w) R.found = true;
+    return true;
+}
+
+// the reference's float64 sample at lattice index k (march_sample, with its
+// own empty-space jump)
+template <typename T>
+__device__ __forceinline__ void fx_exact_step(const Ctx<T>& C, const vc_render_params& P, RayState& R,
+                                              const FxLanes& S, int me, int& k, unsigned& nsamp, unsigned& nskip) {
+    Ctx<T> Cx = C;
+    Cx.rp = fx_rp(C.rp, S, me);
+    const double base = S.base[me];
+    const double t = dadd(base, dmul((double)k, P.coarse));
+    double p[3];
+    Cx.rp.at(t, p);
+    double kd = (double)k;
+    const int w = march_sample<T, VC_TRILINEAR, true>(Cx, P, p, t, kd, base, nskip);
+    if (w < 0) {
+        k = (int)kd;
+        return;
+    }
+    nsamp++;
+    k++;
+    if (w) R.found = true;
+}
+
+// window test of a fixed-point position whose float64 parameter is t
+template <typename T>
+__device__ __forceinline__ bool window_fx(const Ctx<T>& C, const vc_render_params& P, const FxLanes& S, int me,
+                                          const long long q[3], double t, bool ok) {
+    bool g = !ok;
+    const int ci = fx_cell(q[0]), cj = fx_cell(q[1]), ck = fx_cell(q[2]);
+    const float fx = fx_frac(q[0], g), fy = fx_frac(q[1], g), fz = fx_frac(q[2], g);
+    int w = -1;
+    if (!g) {
+        const bool inr = (unsigned)ci < (unsigned)(C.v.nx - 1) && (unsigned)cj < (unsigned)(C.v.ny - 1) &&
+                         (unsigned)ck < (unsigned)(C.v.nz - 1);
+        if (!inr) return in_window(P, 0.0);
+        w = window_cell_f<T>(C.v, ci, cj, ck, fx, fy, fz, C.sk.win);
+    }
+    if (w >= 0) return w != 0;
+    const RayPos rp = fx_rp(C.rp, S, me);
+    double p[3];
+    rp.at(t, p);
+    return window_at<T, VC_TRILINEAR>(C, P, p);
+}
+
+// refine_hit on the fixed-point walk from the hit at lattice index khit:
+// the fine lattice t - j*fine is p_hit - j*DF, the bisection midpoints
+// (qa + qb) >> 1; every t is still formed in float64 exactly as the
+// reference does (the result t_star and the float64 fallbacks use it)
+template <typename T>
+__device__ __forceinline__ double refine_hit_fx(const Ctx<T>& C, const vc_render_params& P, const FxLanes& S,
+                                                int me, int khit, unsigned& nsamp) {
+    const double t = dadd(S.base[me], dmul((double)khit, P.coarse));
+    const double fine = P.fine;
+    long long q[3], df[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        const long long dp = S.dp[a][me];
+        q[a] = fx_at(S.p0[a][me], dp, khit);
+        // dp == 0: a ray fx_setup did not admit (its fractions stay at 0)
+        df[a] = dp != 0 ? to_fx(dmul(dmul(fine, S.d[a][me]), C.rp.rs[a])) : 0;
+    }
+    bool bracket = false;
+    double t_in = t, t_before = t;
+    const double floor_t = dsub(S.t_enter[me], 1e-12);
+    int jj = 0;
+    for (double j = 1.0;; j += 1.0) {
+        const double tb = dsub(t, dmul(j, fine));
+        if (tb < floor_t) {
+            t_in = t_before = dsub(t, dmul(j - 1.0, fine));
+            break;
+        }
+#pragma unroll
+        for (int a = 0; a < 3; a++) q[a] -= df[a];
+        jj++;
+        nsamp++;
+        if (!window_fx<T>(C, P, S, me, q, tb, jj < (1 << 18))) {
+            t_in = dsub(t, dmul(j - 1.0, fine));
+            t_before = tb;
+            bracket = true;
+            break;
+        }
+    }
+    double tcur = t_in;
+    if (bracket && P.refine_iters > 0) {
+        const bool okb = P.refine_iters <= 64;
+        long long qa[3];  // q: the out-of-window end, qa: the in-window end
+#pragma unroll
+        for (int a = 0; a < 3; a++) qa[a] = q[a] + df[a];
+        double tb = t_before, ta = t_in;
+        for (int it = 0; it < P.refine_iters; it++) {
+            const double tm = dmul(0.5, dadd(tb, ta));
+            long long qm[3];
+#pragma unroll
+            for (int a = 0; a < 3; a++) qm[a] = (qa[a] + q[a]) >> 1;
+            nsamp++;
+            const bool in = window_fx<T>(C, P, S, me, qm, tm, okb);
+#pragma unroll
+            for (int a = 0; a < 3; a++) {
+                qa[a] = in ? qm[a] : qa[a];
+                q[a] = in ? q[a] : qm[a];
+            }
+            if (in) ta = tm;
+            else tb = tm;
+        }
+        tcur = ta;
+    }
+    return tcur;
+}
+
 __device__ __forceinline__ uchar4 composite_pixel(const vc_render_params& P, const RayState& R) {
     return make_uchar4(quant(dadd(R.acc_r, dmul(R.remain, P.bg[0]))),
                        quant(dadd(R.acc_g, dmul(R.remain, P.bg[1]))),
@@ -849,6 +1159,7 @@ __device__ __forceinline__ void init_ctx(Ctx<T>& C, const vc_render_params& P, c
     C.sk.my = my;
     C.sk.on = skip_on != 0;
     C.sk.inv_coarse = 1.0 / P.coarse;
+    C.sk.inv_coarse_f = (float)C.sk.inv_coarse;
     C.sk.win = make_winf(P.t_low, P.t_high, vol.amax);
     C.lut = nullptr;
 }
@@ -903,7 +1214,7 @@ __device__ __forceinline__ unsigned warp_ticket(unsigned* ctr, bool want) {
 #define VC_SHV_MINB 7
 #endif
 
-template <typename T, int INTERP>
+template <typename T, int INTERP, bool FXW>
 __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
                                                           RayPos rp0, const uint8_t* __restrict__ dist, int mx,
                                                           int my, int skip_on, PixelSink sink,
@@ -917,6 +1228,12 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
     init_ctx(C, P, vol, nullptr, rp0, dist, mx, my, skip_on, tex);
     unsigned nsamp = 0, nshade = 0, nskip = 0, nhit = 0;
     RayState R;
+    // FXW: the fixed-point walk (trilinear sampling without the adaptive stride)
+    constexpr bool fxw = FXW && INTERP == VC_TRILINEAR;
+    __shared__ FxLanes fxs;
+    const int me = threadIdx.x;
+    int kf = 0;         // lattice index of the fixed-point walk
+    bool pend = false;  // paused for a float64 sample (fx_exact_step)
     int px = 0, lr = 0;
     bool active = false, done = false;
     for (;;) {
@@ -935,6 +1252,10 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
                         if (start_ray(C, P, px, image_row(P, lr), R)) {
                             active = true;
                             nhit++;
+                            if constexpr (fxw) {
+                                fx_setup(C, P, R, fxs, me);
+                                kf = 0;
+                            }
                         } else {
                             put_pixel(sink, P, lr, px, bg_pixel(P));
                         }
@@ -943,27 +1264,51 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
             }
         }
         if (__all_sync(FULL, done)) break;
-        for (;;) {
-            const bool need = active && !R.found && !R.exhausted;
-            const unsigned mneed = __ballot_sync(FULL, need);
-            if (mneed == 0) break;
-            if (VC_FH_READY < READY_DEN) {  // (at READY_DEN the mneed == 0 exit above is the rule)
-                const unsigned mact = __ballot_sync(FULL, active);
-                if (__popc(mact & ~mneed) * READY_DEN >= __popc(mact) * VC_FH_READY) break;
+        if constexpr (fxw) {
+            for (;;) {  // march phases: the walk in registers, float64 samples in between
+                const FxRay F = fx_load(fxs, me);
+                for (;;) {
+                    const bool need = active && !R.found && !R.exhausted && !pend;
+                    if (__ballot_sync(FULL, need) == 0) break;
+                    if (need) pend = !march_step_fx<T>(C, P, R, F, kf, nsamp, nskip);
+                }
+                if (__ballot_sync(FULL, pend) == 0) break;
+                if (pend) {
+                    fx_exact_step<T>(C, P, R, fxs, me, kf, nsamp, nskip);
+                    pend = false;
+                }
             }
-            if (need) march_step<T, INTERP>(C, P, R, nsamp, nskip, P.use_adaptive ? &oct : nullptr);
+        } else {
+            for (;;) {
+                const bool need = active && !R.found && !R.exhausted;
+                const unsigned mneed = __ballot_sync(FULL, need);
+                if (mneed == 0) break;
+                if (VC_FH_READY < READY_DEN) {  // (at READY_DEN the mneed == 0 exit above is the rule)
+                    const unsigned mact = __ballot_sync(FULL, active);
+                    if (__popc(mact & ~mneed) * READY_DEN >= __popc(mact) * VC_FH_READY) break;
+                }
+                if (need) march_step<T, INTERP, true>(C, P, R, nsamp, nskip, P.use_adaptive ? &oct : nullptr);
+            }
         }
         const bool hit = active && R.found;
         double t_star = 0.0;
-        if (hit) t_star = refine_hit<T, INTERP>(C, P, R, R.t_hit, nsamp);
+        if (hit) {
+            if constexpr (fxw) t_star = refine_hit_fx<T>(C, P, fxs, me, kf - 1, nsamp);
+            else t_star = refine_hit<T, INTERP>(C, P, R, R.t_hit, nsamp);
+        }
         const unsigned q = warp_ticket(&work->hits, hit);
         if (hit) {
             HitEntry e;
             e.t_star = t_star;
-            e.lim = R.lim;
-            e.d[0] = C.rp.d[0];
-            e.d[1] = C.rp.d[1];
-            e.d[2] = C.rp.d[2];
+            if constexpr (fxw) {
+                e.lim = fxs.lim[me];
+#pragma unroll
+                for (int a = 0; a < 3; a++) e.d[a] = fxs.d[a][me];
+            } else {
+                e.lim = R.lim;
+#pragma unroll
+                for (int a = 0; a < 3; a++) e.d[a] = C.rp.d[a];
+            }
             e.pix = pack_pix(lr, px);
             e.pad = 0u;
             if (vc_st_ok(hits + q, sizeof(HitEntry))) hits[q] = e;
@@ -1437,7 +1782,12 @@ static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
                 *L.p, vol, L.rp, sink, L.local_rows, reinterpret_cast<unsigned long long*>(L.counters), fw,
                 hits, L.oct);
     } else {
-        firsthit_kernel<T, INTERP><<<persistent_blocks(firsthit_kernel<T, INTERP>, (tiles + 3) / 4), 128, 0, stream>>>(
+        // the fixed-point walk: trilinear sampling without the adaptive stride
+        auto k = firsthit_kernel<T, INTERP, false>;
+        if constexpr (INTERP == VC_TRILINEAR) {
+            if (!L.p->use_adaptive) k = firsthit_kernel<T, INTERP, true>;
+        }
+        k<<<persistent_blocks(k, (tiles + 3) / 4), 128, 0, stream>>>(
             *L.p, vol, L.rp, L.occ, L.mx, L.my, L.skip_on, sink, L.local_rows,
             reinterpret_cast<unsigned long long*>(L.counters), fw, hits, L.oct, tex);
     }

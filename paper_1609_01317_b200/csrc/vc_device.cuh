@@ -449,6 +449,58 @@ __device__ __forceinline__ bool in_window_corners(const wide_t<T> c[8], const Lo
     return t_low <= val && val <= t_high;
 }
 
+// the float32 pre-test alone, from float32 fractions: 0 out, 1 in, -1
+// ambiguous (the caller re-evaluates with the reference's float64 cascade)
+template <typename T>
+__device__ __forceinline__ int window_corners_f(const wide_t<T> c[8], float fx, float fy, float fz, const WinF& w) {
+    auto l32 = [](float a, float bb, float t) { return __fmaf_rn(bb - a, t, a); };
+    const float y0 = l32(l32(vox_f32<T>(c[0]), vox_f32<T>(c[1]), fx), l32(vox_f32<T>(c[2]), vox_f32<T>(c[3]), fx), fy);
+    const float y1 = l32(l32(vox_f32<T>(c[4]), vox_f32<T>(c[5]), fx), l32(vox_f32<T>(c[6]), vox_f32<T>(c[7]), fx), fy);
+    const float v32 = l32(y0, y1, fz);
+    if (v32 < w.lo_out || v32 > w.hi_out) return 0;
+    if (v32 >= w.lo_in && v32 <= w.hi_in) return 1;
+    return -1;
+}
+
+// window_corners_f of interior cell (i, j, k): i < nx-1, j < ny-1, k < nz-1
+// (no one-voxel-axis case).  Integer voxels: the x-lerp's left value and
+// the pair difference each come from one integer op + one FADD (magic
+// 2^23 / 1.5 * 2^23 biases, exact for |value| < 2^22).
+template <typename T>
+__device__ __forceinline__ int window_cell_f(const Vol<T>& v, int i, int j, int k, float fx, float fy, float fz,
+                                             const WinF& w) {
+    const uint32_t idx = ((uint32_t)k * (uint32_t)v.ny + (uint32_t)j) * (uint32_t)v.nx + (uint32_t)i;
+    const T* p0 = v.data + idx;
+    const T* p1 = reinterpret_cast<const T*>(reinterpret_cast<const char*>(p0) + v.syb);
+    const T* p2 = reinterpret_cast<const T*>(reinterpret_cast<const char*>(p0) + v.szb);
+    const T* p3 = reinterpret_cast<const T*>(reinterpret_cast<const char*>(p2) + v.syb);
+    const wide_t<T> c0 = vc_ldg(p0), c1 = vc_ldg(p0 + 1), c2 = vc_ldg(p1), c3 = vc_ldg(p1 + 1);
+    const wide_t<T> c4 = vc_ldg(p2), c5 = vc_ldg(p2 + 1), c6 = vc_ldg(p3), c7 = vc_ldg(p3 + 1);
+    float x0, x1, x2, x3;
+    if constexpr (VoxelBits<T>::integral) {
+        auto left = [](wide_t<T> a) { return __fsub_rn(__int_as_float(0x4B000000 + (int)a), 8388608.0f); };
+        auto diff = [](wide_t<T> a, wide_t<T> b) {
+            return __fsub_rn(__int_as_float((int)b - (int)a + 0x4B400000), 12582912.0f);
+        };
+        x0 = __fmaf_rn(diff(c0, c1), fx, left(c0));
+        x1 = __fmaf_rn(diff(c2, c3), fx, left(c2));
+        x2 = __fmaf_rn(diff(c4, c5), fx, left(c4));
+        x3 = __fmaf_rn(diff(c6, c7), fx, left(c6));
+    } else {
+        auto l32 = [](float a, float bb, float t) { return __fmaf_rn(bb - a, t, a); };
+        x0 = l32(c0, c1, fx);
+        x1 = l32(c2, c3, fx);
+        x2 = l32(c4, c5, fx);
+        x3 = l32(c6, c7, fx);
+    }
+    const float y0 = __fmaf_rn(x1 - x0, fy, x0);
+    const float y1 = __fmaf_rn(x3 - x2, fy, x2);
+    const float v32 = __fmaf_rn(y1 - y0, fz, y0);
+    if (v32 < w.lo_out || v32 > w.hi_out) return 0;
+    if (v32 >= w.lo_in && v32 <= w.hi_in) return 1;
+    return -1;
+}
+
 template <typename T>
 __device__ __forceinline__ bool in_window_trilinear(const Vol<T>& v, const Loc& L, double t_low, double t_high,
                                                     const WinF& w) {
