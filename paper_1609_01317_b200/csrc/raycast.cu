@@ -711,6 +711,9 @@ __device__ __forceinline__ double refine_hit(const Ctx<T>& C, const vc_render_pa
 //     distance is formed in float32 from the cell, the fraction and a
 //     2^-8 voxel margin (float32 error <= 5e-4 voxel over a 1016-voxel box).
 constexpr double FX_ONE = 0x1p40;
+#ifndef VC_FX_UNROLL2
+#define VC_FX_UNROLL2 1
+#endif
 
 // Per-lane walk state.  It lives in shared memory (structure of arrays: a
 // warp's accesses are conflict-free) and is loaded into registers at the
@@ -925,6 +928,27 @@ __device__ __forceinline__ bool window_fx(const Ctx<T>& C, const vc_render_param
     return window_at<T, VC_TRILINEAR>(C, P, p);
 }
 
+// window_fx through a cell cache (the bisection)
+template <typename T>
+__device__ __forceinline__ bool window_fx_cached(const Ctx<T>& C, const vc_render_params& P, const FxLanes& S,
+                                                 int me, const long long q[3], double t, bool ok, CellCache& cc) {
+    bool g = !ok;
+    const int ci = fx_cell(q[0]), cj = fx_cell(q[1]), ck = fx_cell(q[2]);
+    const float fx = fx_frac(q[0], g), fy = fx_frac(q[1], g), fz = fx_frac(q[2], g);
+    int w = -1;
+    if (!g) {
+        const bool inr = (unsigned)ci < (unsigned)(C.v.nx - 1) && (unsigned)cj < (unsigned)(C.v.ny - 1) &&
+                         (unsigned)ck < (unsigned)(C.v.nz - 1);
+        if (!inr) return in_window(P, 0.0);
+        w = window_cell_cached<T>(C.v, ci, cj, ck, fx, fy, fz, C.sk.win, cc);
+    }
+    if (w >= 0) return w != 0;
+    const RayPos rp = fx_rp(C.rp, S, me);
+    double p[3];
+    rp.at(t, p);
+    return window_at<T, VC_TRILINEAR>(C, P, p);
+}
+
 // refine_hit on the fixed-point walk from the hit at lattice index khit:
 // the fine lattice t - j*fine is p_hit - j*DF, the bisection midpoints
 // (qa + qb) >> 1; every t is still formed in float64 exactly as the
@@ -970,13 +994,16 @@ __device__ __forceinline__ double refine_hit_fx(const Ctx<T>& C, const vc_render
 #pragma unroll
         for (int a = 0; a < 3; a++) qa[a] = q[a] + df[a];
         double tb = t_before, ta = t_in;
+        CellCache cc;
+        cc.i = -1;
+        cc.j = cc.k = 0;
         for (int it = 0; it < P.refine_iters; it++) {
             const double tm = dmul(0.5, dadd(tb, ta));
             long long qm[3];
 #pragma unroll
             for (int a = 0; a < 3; a++) qm[a] = (qa[a] + q[a]) >> 1;
             nsamp++;
-            const bool in = window_fx<T>(C, P, S, me, qm, tm, okb);
+            const bool in = window_fx_cached<T>(C, P, S, me, qm, tm, okb, cc);
 #pragma unroll
             for (int a = 0; a < 3; a++) {
                 qa[a] = in ? qm[a] : qa[a];
@@ -1270,7 +1297,12 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
                 for (;;) {
                     const bool need = active && !R.found && !R.exhausted && !pend;
                     if (__ballot_sync(FULL, need) == 0) break;
-                    if (need) pend = !march_step_fx<T>(C, P, R, F, kf, nsamp, nskip);
+                    if (need) {  // two steps per trip: half the vote / reconvergence overhead
+                        pend = !march_step_fx<T>(C, P, R, F, kf, nsamp, nskip);
+#if VC_FX_UNROLL2
+                        if (!pend && !R.found && !R.exhausted) pend = !march_step_fx<T>(C, P, R, F, kf, nsamp, nskip);
+#endif
+                    }
                 }
                 if (__ballot_sync(FULL, pend) == 0) break;
                 if (pend) {

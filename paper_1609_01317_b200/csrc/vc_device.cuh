@@ -501,6 +501,48 @@ __device__ __forceinline__ int window_cell_f(const Vol<T>& v, int i, int j, int 
     return -1;
 }
 
+// window_cell_f with the cell's x-lerp operands cached across calls
+// (bisection: successive positions almost always share the cell)
+struct CellCache {
+    int i, j, k;
+    float l[4], d[4];  // x-lerp left value and pair difference, four x-edges
+};
+
+template <typename T>
+__device__ __forceinline__ int window_cell_cached(const Vol<T>& v, int i, int j, int k, float fx, float fy, float fz,
+                                                  const WinF& w, CellCache& cc) {
+    if (i != cc.i || j != cc.j || k != cc.k) {
+        const uint32_t idx = ((uint32_t)k * (uint32_t)v.ny + (uint32_t)j) * (uint32_t)v.nx + (uint32_t)i;
+        const T* p0 = v.data + idx;
+        const T* p1 = reinterpret_cast<const T*>(reinterpret_cast<const char*>(p0) + v.syb);
+        const T* p2 = reinterpret_cast<const T*>(reinterpret_cast<const char*>(p0) + v.szb);
+        const T* p3 = reinterpret_cast<const T*>(reinterpret_cast<const char*>(p2) + v.syb);
+        const T* row[4] = {p0, p1, p2, p3};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            const wide_t<T> a = vc_ldg(row[e]), b = vc_ldg(row[e] + 1);
+            if constexpr (VoxelBits<T>::integral) {
+                cc.l[e] = __fsub_rn(__int_as_float(0x4B000000 + (int)a), 8388608.0f);
+                cc.d[e] = __fsub_rn(__int_as_float((int)b - (int)a + 0x4B400000), 12582912.0f);
+            } else {
+                cc.l[e] = a;
+                cc.d[e] = b - a;
+            }
+        }
+        cc.i = i;
+        cc.j = j;
+        cc.k = k;
+    }
+    const float x0 = __fmaf_rn(cc.d[0], fx, cc.l[0]), x1 = __fmaf_rn(cc.d[1], fx, cc.l[1]);
+    const float x2 = __fmaf_rn(cc.d[2], fx, cc.l[2]), x3 = __fmaf_rn(cc.d[3], fx, cc.l[3]);
+    const float y0 = __fmaf_rn(x1 - x0, fy, x0);
+    const float y1 = __fmaf_rn(x3 - x2, fy, x2);
+    const float v32 = __fmaf_rn(y1 - y0, fz, y0);
+    if (v32 < w.lo_out || v32 > w.hi_out) return 0;
+    if (v32 >= w.lo_in && v32 <= w.hi_in) return 1;
+    return -1;
+}
+
 template <typename T>
 __device__ __forceinline__ bool in_window_trilinear(const Vol<T>& v, const Loc& L, double t_low, double t_high,
                                                     const WinF& w) {
