@@ -1698,6 +1698,9 @@ __global__ void __launch_bounds__(128, GV ? VC_SHV_MINB : VC_SH_MINB) shade_kern
     RayState R;
     int px = 0, lr = 0;
     bool active = false, done = false;
+#ifdef VC_DEBUG_RAYCOST
+    unsigned dbg_march = 0, dbg_shade = 0;  // per-ray work, written as the pixel (tools/raycost_probe.py)
+#endif
     for (;;) {
         // refill: a fresh lane starts "found" at its t_star, so its first
         // shade joins the other lanes' shades in the single resolve step below
@@ -1727,6 +1730,9 @@ __global__ void __launch_bounds__(128, GV ? VC_SHV_MINB : VC_SH_MINB) shade_kern
                     R.found = true;
                     R.exhausted = false;
                     active = true;
+#ifdef VC_DEBUG_RAYCOST
+                    dbg_march = dbg_shade = 0;
+#endif
                 }
             }
         }
@@ -1738,6 +1744,9 @@ __global__ void __launch_bounds__(128, GV ? VC_SHV_MINB : VC_SH_MINB) shade_kern
             const unsigned mact = __ballot_sync(FULL, active);
             if (__popc(mact & ~mneed) * READY_DEN >= __popc(mact) * (GV ? VC_SHV_READY : VC_SH_READY)) break;
             if (need) march_step<T, INTERP, true>(C, P, R, nsamp, nskip);
+#ifdef VC_DEBUG_RAYCOST
+            if (need) dbg_march++;
+#endif
         }
         if (active && (R.found || R.exhausted)) {
             uchar4 o;
@@ -1748,8 +1757,14 @@ __global__ void __launch_bounds__(128, GV ? VC_SHV_MINB : VC_SH_MINB) shade_kern
             } else {
                 R.found = false;
                 fin = shade_and_composite<T, OP, INTERP, GV>(C, P, R, R.t_hit, o, nshade);
+#ifdef VC_DEBUG_RAYCOST
+                dbg_shade++;
+#endif
             }
             if (fin) {
+#ifdef VC_DEBUG_RAYCOST
+                o = make_uchar4(dbg_march & 255u, (dbg_march >> 8) & 255u, dbg_shade & 255u, (dbg_shade >> 8) & 255u);
+#endif
                 put_pixel(sink, P, lr, px, o);
                 active = false;
             }
