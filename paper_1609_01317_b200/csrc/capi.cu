@@ -63,6 +63,7 @@ struct vc_volume {
         size_t tile_cap = 0;
         cudaEvent_t done = nullptr;  // recorded after each render that used it
         uint64_t stamp = 0;
+        unsigned seq = 0;            // hit-entry tag of the last render (0: none yet)
     };
     std::unordered_map<cudaStream_t, StreamScratch> scratch;
     uint64_t scratch_clock = 0;
@@ -473,7 +474,18 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
             cudaError_t e = cudaMalloc(&sc.hits, need * vc::hit_entry_bytes());
             if (e != cudaSuccess) return fail(VC_ERR_NOMEM, std::string("cudaMalloc(hit queue): ") + cudaGetErrorString(e));
             sc.hit_cap = need;
+            sc.seq = 0;
         }
+        // hit entries carry the render's tag (kernel B reads an entry once it
+        // holds this render's tag): a fresh queue, or a tag counter about to
+        // wrap, starts from zeroed entries
+        if (sc.seq == 0 || sc.seq == 0xffffffffu) {
+            VC_CUDA(cudaMemsetAsync(sc.hits, 0, sc.hit_cap * vc::hit_entry_bytes(), s));
+            sc.seq = 0;
+        }
+        L.seq = ++sc.seq;
+        static const bool no_overlap = getenv("VC_NO_STAGE_OVERLAP") != nullptr;
+        L.overlap_stages = no_overlap ? 0 : 1;
         L.work = sc.work;
         L.hits = sc.hits;
         // tile pushes need whole 8x4 tiles inside one band (band_rows % 4 == 0)

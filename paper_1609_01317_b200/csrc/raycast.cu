@@ -432,9 +432,10 @@ __device__ __forceinline__ Rgba shade_sample(const Ctx<T>& C, const vc_render_pa
         if (GV) atomicAdd(&g_debug_taps, 1u);
 #endif
         constexpr int SI = INTERP == VC_TEX ? VC_TRILINEAR : INTERP;  // boundary band: software value
-        // the general taps loop rolled except in the integer-grid
-        // gradient-volume kernels (grad_raw: register pressure vs icache)
-        constexpr bool ROLL = !GV || !std::is_integral<T>::value;
+        // the general 26-tap loop rolled except in the integer-grid
+        // gradient-volume kernels (grad_raw: register pressure vs icache);
+        // central differences' 6 taps stay unrolled (small code)
+        constexpr bool ROLL = (!GV || !std::is_integral<T>::value) && grad_samples(OP) > 6;
         if constexpr (GV) {  // the rare path of the gradient-volume kernel: out of line
             const double2 iv = taps_illum_value<T, OP, SI, ROLL>(C.v, p[0], p[1], p[2], wx, wy, wz, P.light_pos[0],
                                                                  P.light_pos[1], P.light_pos[2]);
@@ -1162,13 +1163,109 @@ struct __align__(16) HitEntry {
 static_assert(sizeof(HitEntry) == 48, "hit queue entry layout");
 __device__ __forceinline__ uint32_t pack_pix(int lr, int px) { return ((uint32_t)lr << 16) | (uint32_t)px; }
 
+#ifndef VC_STAGE_OVERLAP
+#define VC_STAGE_OVERLAP 1
+#endif
+
 // Work counters of one launch pair (zeroed together before the frame).
 struct FrameWork {
-    unsigned pixels;  // kernel A: next pixel work item
-    unsigned hits;    // kernel A -> B: queue length
-    unsigned shades;  // kernel B: next queue entry
-    unsigned pad;
+    unsigned pixels;   // kernel A: next pixel work item
+    unsigned hits;     // kernel A -> B: queue length (tickets taken)
+    unsigned shades;   // kernel B: next queue entry
+    unsigned fh_done;  // kernel A warps finished (queue length final when all are)
 };
+
+// Stage hand-off.  Kernel B is launched with programmatic stream
+// serialization and kernel A lets it start at once (griddepcontrol), so B's
+// blocks take the SMs A's blocks leave during A's tail.  A hit entry is
+// published by a release store of the frame's tag into its last word after
+// the payload.  B reads the tag with a strong (L2) load and, once it holds
+// this frame's tag, the payload with L1-bypassing loads issued under that
+// branch: the release made the payload visible at L2, the point of
+// coherence, before the tag.  (An acquire load would order it in the PTX
+// model too, but it invalidates the SM's whole L1 -- CCTL.IVALL -- on every
+// refill, which cost the gradient-volume and tap gathers 7-9%.)  B's lane
+// with queue ticket q is done when every A block has finished and q is past
+// the final queue length.  Without the overlap (ncu replay, an event between
+// the launches) every tag is already there and nothing waits.
+__device__ __forceinline__ unsigned ld_strong_u32(const unsigned* p) {
+#ifdef VC_CHECKED
+    if (!vc_addr_ok(p, sizeof(unsigned))) return 0u;
+#endif
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// a published entry's payload, from L2
+__device__ __forceinline__ HitEntry load_hit(const HitEntry* p) {
+    HitEntry e;
+#ifdef VC_CHECKED
+    if (!vc_addr_ok(p, sizeof(HitEntry))) return HitEntry{};
+#endif
+    const uint4* s = reinterpret_cast<const uint4*>(p);
+    uint4* d = reinterpret_cast<uint4*>(&e);
+    d[0] = __ldcg(s);
+    d[1] = __ldcg(s + 1);
+    d[2] = __ldcg(s + 2);
+    return e;
+}
+
+// kernel B's refill while kernel A may still run: is every A block done
+// (warp-uniform; then the final queue length), else is this lane's entry
+// published.  st: 0 keep waiting, 1 claim, 2 past the end of the queue.
+struct OverlapPoll {
+    int st;
+    bool fh_all;
+    unsigned final_hits;
+};
+__device__ __noinline__ OverlapPoll overlap_poll(const FrameWork* work, const HitEntry* hits, unsigned nfh,
+                                                 unsigned seq, unsigned max_hits, unsigned qt, bool waiting,
+                                                 unsigned spin) {
+    const unsigned FULL = 0xffffffffu;
+    unsigned f = 0u, h = 0u;
+    if ((threadIdx.x & 31) == 0) {
+        f = ld_strong_u32(&work->fh_done);
+        if (f >= nfh) h = ld_strong_u32(&work->hits);
+    }
+    f = __shfl_sync(FULL, f, 0);
+    h = __shfl_sync(FULL, h, 0);
+    OverlapPoll r{0, f >= nfh, h};
+    if (!waiting) return r;
+    if (r.fh_all) r.st = qt < h ? 1 : 2;
+    else if (qt < max_hits && ld_strong_u32(&hits[qt].pad) == seq) r.st = 1;
+    else if (spin >= (1u << 24)) r.st = 2;  // safety net: never hang the device on a lost entry
+    return r;
+}
+
+// release: kernel B may read the queue while kernel A runs (overlap on)
+__device__ __forceinline__ void publish_hit(HitEntry* hits, unsigned q, HitEntry e, unsigned seq, bool release) {
+    HitEntry* d = hits + q;
+    if (!vc_st_ok(d, sizeof(HitEntry))) return;
+    if (release) {
+        e.pad = 0u;
+        *d = e;
+        st_release_u32(&d->pad, seq);
+    } else {
+        e.pad = seq;
+        *d = e;
+    }
+}
+
+// end of a kernel-A warp: its hits are published, count it (kernel B
+// expects 4 per block)
+__device__ __forceinline__ void firsthit_block_done(FrameWork* work) {
+    __syncwarp();
+    // a release add, not __threadfence + atomicAdd: a full fence invalidates
+    // the SM's L1 under the warps still marching (measured 2%)
+    if ((threadIdx.x & 31) == 0 && vc_st_ok(&work->fh_done, sizeof(unsigned)))
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&work->fh_done) : "memory");
+}
+
+__device__ __forceinline__ void allow_dependent_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 template <typename T>
 __device__ __forceinline__ void init_ctx(Ctx<T>& C, const vc_render_params& P, const Vol<T>& vol,
@@ -1247,7 +1344,8 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
                                                           int my, int skip_on, PixelSink sink,
                                                           int local_rows, unsigned long long* counters,
                                                           FrameWork* work, HitEntry* __restrict__ hits,
-                                                          OctDev oct, TexArgs tex) {
+                                                          OctDev oct, TexArgs tex, unsigned seq, int rel) {
+    if (rel) allow_dependent_launch();
     const unsigned FULL = 0xffffffffu;
     const int tiles_x = (P.width + 7) >> 3;
     const unsigned total = (unsigned)tiles_x * (unsigned)((local_rows + 3) >> 2) * 32u;
@@ -1343,7 +1441,7 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
             }
             e.pix = pack_pix(lr, px);
             e.pad = 0u;
-            if (vc_st_ok(hits + q, sizeof(HitEntry))) hits[q] = e;
+            publish_hit(hits, q, e, seq, rel != 0);
         }
         if (active && (R.found || R.exhausted)) {
             if (R.exhausted) put_pixel(sink, P, lr, px, bg_pixel(P));
@@ -1351,6 +1449,7 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
         }
     }
     commit_counters(counters, 0, nsamp, nshade, nskip, nhit);
+    firsthit_block_done(work);
 }
 
 // use_adaptive with use_octree (raycast.py:494-499, _kernels.py:656): the reference's first
@@ -1569,7 +1668,9 @@ template <typename T, int INTERP>
 __global__ void __launch_bounds__(128) firsthit_seg_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
                                                            RayPos rp0, PixelSink sink, int local_rows,
                                                            unsigned long long* counters, FrameWork* work,
-                                                           HitEntry* __restrict__ hits, OctDev oct) {
+                                                           HitEntry* __restrict__ hits, OctDev oct, unsigned seq,
+                                                           int rel) {
+    if (rel) allow_dependent_launch();
     const unsigned FULL = 0xffffffffu;
     const int tiles_x = (P.width + 7) >> 3;
     const unsigned total = (unsigned)tiles_x * (unsigned)((local_rows + 3) >> 2) * 32u;
@@ -1664,7 +1765,7 @@ __global__ void __launch_bounds__(128) firsthit_seg_kernel(const __grid_constant
             e.d[2] = C.rp.d[2];
             e.pix = pack_pix(lr, px);
             e.pad = 0u;
-            if (vc_st_ok(hits + q, sizeof(HitEntry))) hits[q] = e;
+            publish_hit(hits, q, e, seq, rel != 0);
             active = false;
         }
         if (miss) {
@@ -1673,6 +1774,7 @@ __global__ void __launch_bounds__(128) firsthit_seg_kernel(const __grid_constant
         }
     }
     commit_counters(counters, 0, nsamp, 0, 0, nhit);
+    firsthit_block_done(work);
 }
 
 // Kernel B -- shade + composite (wavefront stage 2).  Persistent CTAs pull
@@ -1686,9 +1788,12 @@ __global__ void __launch_bounds__(128, GV ? VC_SHV_MINB : VC_SH_MINB) shade_kern
                                                        const uint8_t* __restrict__ dist, int mx, int my,
                                                        int skip_on, PixelSink sink,
                                                        unsigned long long* counters, FrameWork* work,
-                                                       const HitEntry* __restrict__ hits, TexArgs tex) {
+                                                       const HitEntry* __restrict__ hits, TexArgs tex,
+                                                       unsigned seq, unsigned nfh, unsigned max_hits) {
     const unsigned FULL = 0xffffffffu;
-    const unsigned total = *(volatile unsigned*)&work->hits;
+    // the overlapped stage hand-off: gradient-volume shading (the taps
+    // kernel keeps the plain refill; measured slower with it, register bound)
+    constexpr bool OV = GV && VC_STAGE_OVERLAP;
     __shared__ SharedLut s_lut;
     load_shared_lut(P, s_lut);
     Ctx<T> C;
@@ -1698,41 +1803,85 @@ __global__ void __launch_bounds__(128, GV ? VC_SHV_MINB : VC_SH_MINB) shade_kern
     RayState R;
     int px = 0, lr = 0;
     bool active = false, done = false;
+    unsigned qt = 0;
+    bool waiting = false;      // OV: holds queue ticket qt, entry not published yet
+    bool fh_all = !OV;         // every kernel-A block has finished (warp-uniform)
+    unsigned final_hits = 0u;  // the queue length then
+    if constexpr (!OV) final_hits = *(volatile unsigned*)&work->hits;
 #ifdef VC_DEBUG_RAYCOST
     unsigned dbg_march = 0, dbg_shade = 0;  // per-ray work, written as the pixel (tools/raycost_probe.py)
 #endif
+    // a lane takes the entry of its ticket: regenerate the ray at t_star
+    auto start = [&](const HitEntry& e) {
+        px = (int)(e.pix & 0xffffu);
+        lr = (int)(e.pix >> 16);
+#pragma unroll
+        for (int a = 0; a < 3; a++) C.rp.d[a] = e.d[a];
+        R.lim = e.lim;
+        R.base = e.t_star;
+        R.k = 1.0;
+        R.acc_r = R.acc_g = R.acc_b = 0.0;
+        R.remain = 1.0;
+        R.t_hit = e.t_star;
+        R.found = true;
+        R.exhausted = false;
+        active = true;
+#ifdef VC_DEBUG_RAYCOST
+        dbg_march = dbg_shade = 0;
+#endif
+    };
     for (;;) {
         // refill: a fresh lane starts "found" at its t_star, so its first
         // shade joins the other lanes' shades in the single resolve step below
         // (only once VC_SH_REFILL lanes are idle, or none is active: each
         // refill stalls the warp on the queue reads)
-        for (;;) {
-            const bool want = !active && !done;
-            const unsigned mw = __ballot_sync(FULL, want);
-            if (mw == 0) break;
-            if (__popc(mw) < VC_SH_REFILL && __ballot_sync(FULL, active) != 0) break;
-            const unsigned q = warp_ticket(&work->shades, want);
-            if (want) {
-                if (q >= total) {
-                    done = true;
-                } else {
-                    const HitEntry e = vc_ld(hits + q);
-                    px = (int)(e.pix & 0xffffu);
-                    lr = (int)(e.pix >> 16);
-#pragma unroll
-                    for (int a = 0; a < 3; a++) C.rp.d[a] = e.d[a];
-                    R.lim = e.lim;
-                    R.base = e.t_star;
-                    R.k = 1.0;
-                    R.acc_r = R.acc_g = R.acc_b = 0.0;
-                    R.remain = 1.0;
-                    R.t_hit = e.t_star;
-                    R.found = true;
-                    R.exhausted = false;
-                    active = true;
-#ifdef VC_DEBUG_RAYCOST
-                    dbg_march = dbg_shade = 0;
-#endif
+        if constexpr (OV) {
+            for (unsigned spin = 0;; spin++) {
+                const bool want = !active && !done && !waiting;
+                const unsigned mw = __ballot_sync(FULL, want);
+                if (mw != 0 && (__popc(mw) >= VC_SH_REFILL || __ballot_sync(FULL, active) == 0)) {
+                    const unsigned q = warp_ticket(&work->shades, want);
+                    if (want) {
+                        qt = q;
+                        waiting = true;
+                    }
+                }
+                if (__ballot_sync(FULL, waiting) == 0) break;
+                bool claim = false;
+                if (!fh_all) {  // kernel A may still be running (out of line: keeps the hot code compact)
+                    const OverlapPoll r = overlap_poll(work, hits, nfh, seq, max_hits, qt, waiting, spin);
+                    fh_all = r.fh_all;
+                    final_hits = r.final_hits;
+                    claim = r.st == 1;
+                    if (r.st == 2) {
+                        waiting = false;
+                        done = true;
+                    }
+                } else if (waiting) {  // the queue is complete: every entry below final_hits is published
+                    claim = qt < final_hits;
+                    if (!claim) {
+                        waiting = false;
+                        done = true;
+                    }
+                }
+                if (claim) {
+                    waiting = false;
+                    start(load_hit(hits + qt));
+                }
+                if (__ballot_sync(FULL, active) != 0 || __all_sync(FULL, done)) break;
+                // nothing to shade yet: lanes wait for entries kernel A is still producing
+                if (__ballot_sync(FULL, waiting) != 0) __nanosleep(spin < 8 ? 256u : 2048u);
+            }
+        } else {
+            for (;;) {
+                const bool want = !active && !done;
+                const unsigned mw = __ballot_sync(FULL, want);
+                if (mw == 0) break;
+                if (__popc(mw) < VC_SH_REFILL && __ballot_sync(FULL, active) != 0) break;
+                const unsigned q = warp_ticket(&work->shades, want);
+                if (want) {
+                    if (q >= final_hits) done = true;
+                    else start(vc_ld(hits + q));
                 }
             }
         }
@@ -1768,6 +1917,7 @@ __global__ void __launch_bounds__(128, GV ? VC_SHV_MINB : VC_SH_MINB) shade_kern
                 put_pixel(sink, P, lr, px, o);
                 active = false;
             }
+
         }
     }
     commit_counters(counters, 1, nsamp, nshade, nskip, nhit);
@@ -1822,35 +1972,52 @@ static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
     // use_adaptive + use_octree, or use_octree with 0 in the window: the
     // octree-segment first hit (exact reference walk, capi.cu render_impl)
     const bool seg = INTERP != VC_TEX && L.seg_walk;
+    unsigned nfh = 0;  // kernel-A blocks (kernel B's end-of-queue test)
+    // the overlapped hand-off: gradient-volume shading, composited frames
+    // (a surface frame's shade stage is too short to gain from it)
+    const int overlap = (VC_STAGE_OVERLAP && L.overlap_stages && L.grad != nullptr && L.p->mode != VC_SURFACE) ? 1 : 0;
     if (seg) {
-        if constexpr (INTERP != VC_TEX)
-            firsthit_seg_kernel<T, INTERP><<<persistent_blocks(firsthit_seg_kernel<T, INTERP>, (tiles + 3) / 4), 128, 0,
-                                             stream>>>(
+        if constexpr (INTERP != VC_TEX) {
+            nfh = persistent_blocks(firsthit_seg_kernel<T, INTERP>, (tiles + 3) / 4);
+            firsthit_seg_kernel<T, INTERP><<<nfh, 128, 0, stream>>>(
                 *L.p, vol, L.rp, sink, L.local_rows, reinterpret_cast<unsigned long long*>(L.counters), fw,
-                hits, L.oct);
+                hits, L.oct, L.seq, overlap);
+        }
     } else {
         // the fixed-point walk: trilinear sampling without the adaptive stride
         auto k = firsthit_kernel<T, INTERP, false>;
         if constexpr (INTERP == VC_TRILINEAR) {
             if (!L.p->use_adaptive) k = firsthit_kernel<T, INTERP, true>;
         }
-        k<<<persistent_blocks(k, (tiles + 3) / 4), 128, 0, stream>>>(
-            *L.p, vol, L.rp, L.occ, L.mx, L.my, L.skip_on, sink, L.local_rows,
-            reinterpret_cast<unsigned long long*>(L.counters), fw, hits, L.oct, tex);
+        nfh = persistent_blocks(k, (tiles + 3) / 4);
+        k<<<nfh, 128, 0, stream>>>(*L.p, vol, L.rp, L.occ, L.mx, L.my, L.skip_on, sink, L.local_rows,
+                                   reinterpret_cast<unsigned long long*>(L.counters), fw, hits, L.oct, tex, L.seq,
+                                   overlap);
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (L.ev[1]) cudaEventRecord(L.ev[1], stream);
     const float4* grad = static_cast<const float4*>(L.grad);
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(L.counters);
-    if (grad != nullptr)
-        shade_kernel<T, OP, INTERP, true><<<persistent_blocks(shade_kernel<T, OP, INTERP, true>, (tiles + 3) / 4),
-                                            128, 0, stream>>>(*L.p, vol, grad, L.rp, L.occ, L.mx, L.my,
-                                                              L.skip_on, sink, cnt, fw, hits, tex);
-    else
-        shade_kernel<T, OP, INTERP, false><<<persistent_blocks(shade_kernel<T, OP, INTERP, false>, (tiles + 3) / 4),
-                                             128, 0, stream>>>(*L.p, vol, grad, L.rp, L.occ, L.mx, L.my,
-                                                               L.skip_on, sink, cnt, fw, hits, tex);
+    // kernel B may start while kernel A finishes (programmatic stream
+    // serialization; see "Stage hand-off")
+    auto launch_b = [&](auto kernel) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(persistent_blocks(kernel, (tiles + 3) / 4));
+        cfg.blockDim = dim3(128);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = overlap;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kernel, *L.p, vol, grad, L.rp, L.occ, L.mx, L.my, L.skip_on, sink, cnt, fw,
+                                  hits, tex, L.seq, nfh * 4u, (unsigned)((long long)L.local_rows * L.p->width));
+    };
+    if (grad != nullptr) e = launch_b(shade_kernel<T, OP, INTERP, true>);
+    else e = launch_b(shade_kernel<T, OP, INTERP, false>);
+    if (e != cudaSuccess) return e;
     if (L.ev[2]) cudaEventRecord(L.ev[2], stream);
     return cudaGetLastError();
 }

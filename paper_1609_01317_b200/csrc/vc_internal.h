@@ -49,6 +49,8 @@ struct RenderLaunch {
     uint64_t* counters;   // VC_NUM_COUNTERS or nullptr
     void* work;           // frame work counters (FrameWork, zeroed per launch)
     void* hits;           // first-hit queue, >= local_rows * width entries
+    unsigned seq;         // this render's hit-entry tag (never 0, unique per scratch until it wraps)
+    int overlap_stages;   // launch the shade kernel with programmatic stream serialization
     cudaEvent_t ev[3];    // optional: recorded before stage 1, between, after stage 2
     OctDev oct;           // adaptive stepping (levels == 0 when unused)
     // VC_SAMPLER_TEXTURE: tex3D objects over cudaArray copies of the grid
