@@ -484,8 +484,16 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
             sc.seq = 0;
         }
         L.seq = ++sc.seq;
+        // overlap the two stages (kernel B starting in kernel A's tail) only
+        // when this render is alone on the device: with renders of other
+        // streams in flight (render_sequence) the tail is filled anyway and
+        // kernel B's early blocks would only poll
         static const bool no_overlap = getenv("VC_NO_STAGE_OVERLAP") != nullptr;
-        L.overlap_stages = no_overlap ? 0 : 1;
+        bool alone = true;
+        for (auto& kv : v->scratch)
+            if (kv.first != s && kv.second.done && cudaEventQuery(kv.second.done) == cudaErrorNotReady) alone = false;
+        if (!alone) (void)cudaGetLastError();  // a not-ready status is not this render's error
+        L.overlap_stages = (!no_overlap && alone) ? 1 : 0;
         L.work = sc.work;
         L.hits = sc.hits;
         // tile pushes need whole 8x4 tiles inside one band (band_rows % 4 == 0)
