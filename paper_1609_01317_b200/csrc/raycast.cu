@@ -502,13 +502,13 @@ __device__ __forceinline__ bool start_ray(Ctx<T>& C, const vc_render_params& P, 
     const double dn = __dsqrt_rn(dadd(dadd(dmul(d[0], d[0]), dmul(d[1], d[1])), dmul(d[2], d[2])));
     const double ydn = rcp_for(dn);
 #pragma unroll
-    for (int a = 0; a < 3; a++) {
-        C.rp.d[a] = div_rcp(d[a], dn, ydn);
-        // skip_to's reciprocal speed: only conservativeness matters (EPS margins)
-        C.sk.ib[a] = C.rp.d[a] == 0.0 ? 0.0 : dmul(C.rp.s[a], __drcp_rn(C.rp.d[a]));
-    }
-    double t_enter, t_exit;
-    if (!box_interval(C.rp.o, C.rp.d, P.clip_lo, P.clip_hi, t_enter, t_exit)) return false;
+    for (int a = 0; a < 3; a++) C.rp.d[a] = div_rcp(d[a], dn, ydn);
+    double t_enter, t_exit, inv[3];
+    if (!box_interval(C.rp.o, C.rp.d, P.clip_lo, P.clip_hi, t_enter, t_exit, inv)) return false;
+    // skip_to's reciprocal speed s / d from the slab test's RN(1 / d) (0 for
+    // d == 0): only conservativeness matters (EPS margins)
+#pragma unroll
+    for (int a = 0; a < 3; a++) C.sk.ib[a] = dmul(C.rp.s[a], inv[a]);
     R.t_enter = t_enter;
     if (t_exit_out != nullptr) *t_exit_out = t_exit;
     R.lim = dadd(t_exit, 1e-12);
@@ -804,7 +804,7 @@ __device__ __forceinline__ void fx_setup(const Ctx<T>& C, const vc_render_params
     for (int a = 0; a < 3; a++) {
         S.p0[a][me] = ok ? to_fx(pb[a]) : 0;
         S.dp[a][me] = ok ? to_fx(dmul(dmul(P.coarse, C.rp.d[a]), C.rp.rs[a])) : 0;
-        S.ibf[a][me] = C.rp.d[a] == 0.0 ? 0.0f : __double2float_rn(dmul(C.rp.s[a], __drcp_rn(C.rp.d[a])));
+        S.ibf[a][me] = __double2float_rn(C.sk.ib[a]);
         S.d[a][me] = C.rp.d[a];
     }
     S.base[me] = R.base;

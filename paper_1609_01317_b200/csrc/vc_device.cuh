@@ -782,15 +782,19 @@ __device__ __forceinline__ void normalize3(const double g[3], double u[3]) {
 }
 
 // _kernels.py:188-224 (slab_interval + box_interval)
+// inv_out (optional): RN(1 / d) per axis, 0 for d == 0 (valid when true is returned)
 __device__ __forceinline__ bool box_interval(const double o[3], const double d[3], const double lo[3],
-                                             const double hi[3], double& t0, double& t1) {
+                                             const double hi[3], double& t0, double& t1,
+                                             double* inv_out = nullptr) {
     double tmin = -1e300, tmax = 1e300;
 #pragma unroll
     for (int a = 0; a < 3; a++) {
+        if (inv_out) inv_out[a] = 0.0;
         if (d[a] == 0.0) {
             if (o[a] < lo[a] || o[a] > hi[a]) return false;
         } else {
             const double inv = __drcp_rn(d[a]);  // = RN(1.0 / d), the reference's value
+            if (inv_out) inv_out[a] = inv;
             double ta = dmul(dsub(lo[a], o[a]), inv);
             double tb = dmul(dsub(hi[a], o[a]), inv);
             if (ta > tb) {
