@@ -490,11 +490,14 @@ __device__ __forceinline__ int image_row(const vc_render_params& P, int lr) {
 
 // ray generation (_kernels.py:639-648) + box interval (:649); false = miss
 template <typename T>
+// rhw (optional): RN(1/width), RN(1/height) computed once per block
 __device__ __forceinline__ bool start_ray(Ctx<T>& C, const vc_render_params& P, int px, int py,
-                                          RayState& R, double* t_exit_out = nullptr) {
+                                          RayState& R, double* t_exit_out = nullptr,
+                                          const double* rhw = nullptr) {
     const double H = (double)P.height, W = (double)P.width;  // integers: never an all-ones significand
-    const double v_ndc = dsub(1.0, ddiv_rcp(dmul(2.0, dadd((double)py, 0.5)), H, __drcp_rn(H)));
-    const double u_ndc = dsub(ddiv_rcp(dmul(2.0, dadd((double)px, 0.5)), W, __drcp_rn(W)), 1.0);
+    const double rW = rhw ? rhw[0] : __drcp_rn(W), rH = rhw ? rhw[1] : __drcp_rn(H);
+    const double v_ndc = dsub(1.0, ddiv_rcp(dmul(2.0, dadd((double)py, 0.5)), H, rH));
+    const double u_ndc = dsub(ddiv_rcp(dmul(2.0, dadd((double)px, 0.5)), W, rW), 1.0);
     const double uw = dmul(u_ndc, P.half_w), vh = dmul(v_ndc, P.half_h);
     double d[3];
 #pragma unroll
@@ -1356,7 +1359,13 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
     // FXW: the fixed-point walk (trilinear sampling without the adaptive stride)
     constexpr bool fxw = FXW && INTERP == VC_TRILINEAR;
     __shared__ FxLanes fxs;
+    __shared__ double s_rhw[2];  // RN(1/width), RN(1/height)
     const int me = threadIdx.x;
+    if (fxw && me == 0) {
+        s_rhw[0] = __drcp_rn((double)P.width);
+        s_rhw[1] = __drcp_rn((double)P.height);
+    }
+    if (fxw) __syncthreads();
     int kf = 0;         // lattice index of the fixed-point walk
     bool pend = false;  // paused for a float64 sample (fx_exact_step)
     int px = 0, lr = 0;
@@ -1374,7 +1383,7 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
                     px = (int)(tile % (unsigned)tiles_x) * 8 + (int)(r & 7u);
                     lr = (int)(tile / (unsigned)tiles_x) * 4 + (int)(r >> 3);
                     if (px < P.width && lr < local_rows) {
-                        if (start_ray(C, P, px, image_row(P, lr), R)) {
+                        if (start_ray(C, P, px, image_row(P, lr), R, nullptr, fxw ? s_rhw : nullptr)) {
                             active = true;
                             nhit++;
                             if constexpr (fxw) {
