@@ -778,9 +778,33 @@ __device__ __forceinline__ float fx_frac(long long x, bool& g) {
     return __fsub_rn(F, 1.0f);
 }
 
+// The admission bound for every ray of the frame at once: a ray's path
+// parameter never exceeds T = 2*Dmax + coarse (Dmax: the eye's distance to
+// the farthest clip-box corner; t_enter, t_exit <= Dmax), so per axis
+// (|o| + 2T|d|)/s <= (|o| + 2T)/s bounds both the reference's rounding
+// scale and the walk's reach; <= 2^21 leaves the per-ray conditions of the
+// analysis above (2^24, 2^22) a 2x-8x margin.  Computed once per block.
+__device__ __forceinline__ bool fx_frame_admits(const vc_render_params& P, const RayPos& rp) {
+    double dmax = 0.0;
+    for (int c = 0; c < 8; c++) {
+        double q = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            const double w = ((c >> a) & 1) ? P.clip_hi[a] : P.clip_lo[a];
+            q += (w - P.eye[a]) * (w - P.eye[a]);
+        }
+        dmax = fmax(dmax, sqrt(q));
+    }
+    const double T = 2.0 * dmax * (1.0 + 0x1p-20) + P.coarse + 1.0;
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < 3; a++) ok = ok && (fabs(P.eye[a]) + 2.0 * T) * fabs(rp.rs[a]) <= 0x1p21;
+    return ok;
+}
+
 template <typename T>
 __device__ __forceinline__ void fx_setup(const Ctx<T>& C, const vc_render_params& P, const RayState& R, FxLanes& S,
-                                         int me) {
+                                         int me, bool frame_ok) {
     bool ok = true;
     double x = dmul(dsub(R.lim, R.base), C.sk.inv_coarse);
     if (!(x < 524288.0)) {
@@ -793,16 +817,9 @@ __device__ __forceinline__ void fx_setup(const Ctx<T>& C, const vc_render_params
 #pragma unroll 1
     while (kl < 524288 && dadd(R.base, dmul((double)(kl + 1), P.coarse)) <= R.lim) kl++;
     S.klast[me] = kl;
+    ok = ok && frame_ok;  // the frame-wide rounding / reach bound (fx_frame_admits)
     double pb[3];
     C.rp.at(R.base, pb);
-    const double tmax = fabs(R.lim) + fabs(R.base) + P.coarse;
-#pragma unroll
-    for (int a = 0; a < 3; a++) {
-        const double sl = dmul(dmul(P.coarse, C.rp.d[a]), C.rp.rs[a]);
-        const double e = (fabs(C.rp.o[a]) + 2.0 * tmax * fabs(C.rp.d[a])) * fabs(C.rp.rs[a]);
-        const double reach = fabs(pb[a]) + (double)(kl + 1) * fabs(sl);
-        ok = ok && e <= 0x1p24 && reach <= 0x1p22;
-    }
 #pragma unroll
     for (int a = 0; a < 3; a++) {
         S.p0[a][me] = ok ? to_fx(pb[a]) : 0;
@@ -1360,10 +1377,12 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
     constexpr bool fxw = FXW && INTERP == VC_TRILINEAR;
     __shared__ FxLanes fxs;
     __shared__ double s_rhw[2];  // RN(1/width), RN(1/height)
+    __shared__ int s_admit;      // fx_frame_admits
     const int me = threadIdx.x;
     if (fxw && me == 0) {
         s_rhw[0] = __drcp_rn((double)P.width);
         s_rhw[1] = __drcp_rn((double)P.height);
+        s_admit = fx_frame_admits(P, rp0) ? 1 : 0;
     }
     if (fxw) __syncthreads();
     int kf = 0;         // lattice index of the fixed-point walk
@@ -1387,7 +1406,7 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
                             active = true;
                             nhit++;
                             if constexpr (fxw) {
-                                fx_setup(C, P, R, fxs, me);
+                                fx_setup(C, P, R, fxs, me, s_admit != 0);
                                 kf = 0;
                             }
                         } else {

@@ -76,10 +76,11 @@ def test_integer_eye_and_unit_steps_every_sample_on_a_lattice_plane():
     _check(vol, sc, st)
 
 
-@pytest.mark.parametrize("dist", [3.0e7, 1.0e6])
+@pytest.mark.parametrize("dist", [3.0e7, 1.0e6, 2.0e5])
 def test_far_eye(dist):
-    """3e7: |o| / s > 2^24, no ray is admitted (float64 path for every
-    sample); 1e6: admitted with a large rounding bound."""
+    """3e7 and 1e6: beyond the frame-wide admission bound ((|o| + 2T) / s <=
+    2^21), every sample takes the float64 path; 2e5: admitted with a large
+    rounding scale."""
     vol = _ct(64)
     c = (32.0, 30.0, 33.0)
     cam = vc.Camera(eye=(c[0] + 0.3 * dist, c[1] + 0.1 * dist, c[2] - dist), target=c,
