@@ -64,6 +64,7 @@ struct vc_volume {
         cudaEvent_t done = nullptr;  // recorded after each render that used it
         uint64_t stamp = 0;
         unsigned seq = 0;            // hit-entry tag of the last render (0: none yet)
+        bool work_dirty = true;      // the work counters need zeroing before the next render
     };
     std::unordered_map<cudaStream_t, StreamScratch> scratch;
     uint64_t scratch_clock = 0;
@@ -466,7 +467,16 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
         if (!sc.done) VC_CUDA(cudaEventCreateWithFlags(&sc.done, cudaEventDisableTiming));
         scp = &sc;
         const size_t need = (size_t)local_rows * p->width;
-        if (sc.work == nullptr) VC_CUDA(cudaMalloc(&sc.work, vc::frame_work_bytes()));
+        if (sc.work == nullptr) {
+            VC_CUDA(cudaMalloc(&sc.work, vc::frame_work_bytes()));
+            sc.work_dirty = true;
+        }
+        // the frame's work counters are reset by its own last kernel; after a
+        // failed render (or on a fresh scratch) they are zeroed here
+        if (sc.work_dirty) {
+            VC_CUDA(cudaMemsetAsync(sc.work, 0, vc::frame_work_bytes(), s));
+            sc.work_dirty = false;
+        }
         if (sc.hit_cap < need) {
             cudaFree(sc.hits);
             sc.hits = nullptr;
@@ -582,7 +592,13 @@ int render_impl(vc_volume* v, const vc_render_params* p, uint8_t* d_rgba, uint64
     L.regions = R.lohi.data();
     L.nregions = (int)(R.lohi.size() / 2);
 #endif
-    VC_CUDA(vc::launch_raycast(L, s));
+    {
+        const cudaError_t le = vc::launch_raycast(L, s);
+        if (le != cudaSuccess) {
+            scp->work_dirty = true;  // the kernels may not have reset the counters
+            VC_CUDA(le);
+        }
+    }
     if (pf && pf->d_done)  // this rank's bands are in every receiver's frame
         VC_CUDA(vc::launch_signal_flags(pf->d_done, pf->n, pf->dest, pf->self, pf->seq, s));
     VC_CUDA(cudaEventRecord(scp->done, s));

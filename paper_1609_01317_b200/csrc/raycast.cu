@@ -1188,11 +1188,15 @@ __device__ __forceinline__ uint32_t pack_pix(int lr, int px) { return ((uint32_t
 #endif
 
 // Work counters of one launch pair (zeroed together before the frame).
+// Zeroed once when the scratch is allocated; afterwards the last kernel-B
+// warp of each frame zeroes it for the next one (no memset launch per frame).
 struct FrameWork {
     unsigned pixels;   // kernel A: next pixel work item
     unsigned hits;     // kernel A -> B: queue length (tickets taken)
     unsigned shades;   // kernel B: next queue entry
     unsigned fh_done;  // kernel A warps finished (queue length final when all are)
+    unsigned sh_done;  // kernel B warps finished (the last one resets the counters)
+    unsigned pad[3];
 };
 
 // Stage hand-off.  Kernel B is launched with programmatic stream
@@ -1949,6 +1953,21 @@ __global__ void __launch_bounds__(128, GV ? VC_SHV_MINB : VC_SH_MINB) shade_kern
         }
     }
     commit_counters(counters, 1, nsamp, nshade, nskip, nhit);
+    // the frame's last kernel-B warp resets the work counters for the next
+    // frame on this scratch: every kernel-A warp has finished (B's lanes end
+    // only after seeing that) and every other B warp has made its last
+    // counter access (its lanes' atomics returned before its count)
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0 && vc_st_ok(work, sizeof(FrameWork))) {
+        const unsigned nw = gridDim.x * (blockDim.x >> 5);
+        if (atomicAdd(&work->sh_done, 1u) + 1u == nw) {
+            work->pixels = 0u;
+            work->hits = 0u;
+            work->shades = 0u;
+            work->fh_done = 0u;
+            work->sh_done = 0u;
+        }
+    }
 }
 
 }  // namespace vc
@@ -1981,8 +2000,7 @@ static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
     const Vol<T> vol = make_vol(static_cast<const T*>(L.data), L.nx, L.ny, L.nz, L.amax);
     FrameWork* fw = reinterpret_cast<FrameWork*>(L.work);
     HitEntry* hits = reinterpret_cast<HitEntry*>(L.hits);
-    cudaError_t e = cudaMemsetAsync(fw, 0, sizeof(FrameWork), stream);
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;  // fw: zero on entry (see FrameWork)
     const long long tiles = (long long)((L.p->width + 7) / 8) * ((L.local_rows + 3) / 4);
     PixelSink sink{reinterpret_cast<uchar4*>(L.out), reinterpret_cast<uchar4* const*>(L.peers), L.npeers,
                    L.peer_self, L.peer_dest, L.tile_cnt, (L.p->width + 7) / 8, L.local_rows};
