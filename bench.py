@@ -976,8 +976,8 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": 2 * args.steps,
-        "gpu_launches_note": "per frame: vc::firsthit_kernel + vc::shade_kernel (+ one cudaMemsetAsync "
-                             "of the work counters)",
+        "gpu_launches_note": "per frame: vc::firsthit_kernel + vc::shade_kernel (the shade kernel starts "
+                             "in the first hit's tail; its last warp resets the work counters, no memset)",
         "clocks": clk.summary(),
         "parity": parity,
         **({"functional_check_only": f"{backend} backend, ranks sharing one GPU"}
