@@ -1081,7 +1081,7 @@ __device__ __forceinline__ bool shade_and_composite(const Ctx<T>& C, const vc_re
 #define VC_SH_REFILL 24
 #endif
 #ifndef VC_SHV_READY  // shade stage, gradient-volume kernel
-#define VC_SHV_READY 8
+#define VC_SHV_READY 1
 #endif
 constexpr int READY_DEN = 32;
 
