@@ -1426,7 +1426,12 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
                 const FxRay F = fx_load(fxs, me);
                 for (;;) {
                     const bool need = active && !R.found && !R.exhausted && !pend;
-                    if (__ballot_sync(FULL, need) == 0) break;
+                    const unsigned mneed = __ballot_sync(FULL, need);
+                    if (mneed == 0) break;
+                    if (VC_FH_READY < READY_DEN) {  // (at READY_DEN the mneed == 0 exit above is the rule)
+                        const unsigned mact = __ballot_sync(FULL, active && !pend);
+                        if (__popc(mact & ~mneed) * READY_DEN >= __popc(mact) * VC_FH_READY) break;
+                    }
                     if (need) {  // two steps per trip: half the vote / reconvergence overhead
                         pend = !march_step_fx<T>(C, P, R, F, kf, nsamp, nskip);
 #if VC_FX_UNROLL2
