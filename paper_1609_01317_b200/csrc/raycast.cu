@@ -1362,7 +1362,7 @@ __device__ __forceinline__ unsigned warp_ticket(unsigned* ctr, bool want) {
 #define VC_SHV_MINB 7
 #endif
 
-template <typename T, int INTERP, bool FXW>
+template <typename T, int INTERP, bool FXW, bool CNT = true>
 __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
                                                           RayPos rp0, const uint8_t* __restrict__ dist, int mx,
                                                           int my, int skip_on, PixelSink sink,
@@ -1485,7 +1485,7 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
             active = false;
         }
     }
-    commit_counters(counters, 0, nsamp, nshade, nskip, nhit);
+    if constexpr (CNT) commit_counters(counters, 0, nsamp, nshade, nskip, nhit);  // (CNT false: counters == nullptr)
     firsthit_block_done(work);
 }
 
@@ -1819,7 +1819,7 @@ __global__ void __launch_bounds__(128) firsthit_seg_kernel(const __grid_constant
 // composited mode, keep marching t_star + m*coarse and shading in-window
 // samples until early ray termination or the ray leaves the box.  Lanes
 // refill from the queue as their pixel finishes.
-template <typename T, int OP, int INTERP, bool GV>
+template <typename T, int OP, int INTERP, bool GV, bool CNT = true>
 __global__ void __launch_bounds__(128, GV ? VC_SHV_MINB : VC_SH_MINB) shade_kernel(const __grid_constant__ vc_render_params P, Vol<T> vol,
                                                        const float4* __restrict__ grad, RayPos rp0,
                                                        const uint8_t* __restrict__ dist, int mx, int my,
@@ -1957,7 +1957,7 @@ __global__ void __launch_bounds__(128, GV ? VC_SHV_MINB : VC_SH_MINB) shade_kern
 
         }
     }
-    commit_counters(counters, 1, nsamp, nshade, nskip, nhit);
+    if constexpr (CNT) commit_counters(counters, 1, nsamp, nshade, nskip, nhit);  // (CNT false: counters == nullptr)
     // the frame's last kernel-B warp resets the work counters for the next
     // frame on this scratch: every kernel-A warp has finished (B's lanes end
     // only after seeing that) and every other B warp has made its last
@@ -2038,7 +2038,9 @@ static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
         // the fixed-point walk: trilinear sampling without the adaptive stride
         auto k = firsthit_kernel<T, INTERP, false>;
         if constexpr (INTERP == VC_TRILINEAR) {
-            if (!L.p->use_adaptive) k = firsthit_kernel<T, INTERP, true>;
+            // the fixed-point walk; without work counters the counting compiles out
+            if (!L.p->use_adaptive)
+                k = L.counters ? firsthit_kernel<T, INTERP, true, true> : firsthit_kernel<T, INTERP, true, false>;
         }
         nfh = persistent_blocks(k, (tiles + 3) / 4);
         k<<<nfh, 128, 0, stream>>>(*L.p, vol, L.rp, L.occ, L.mx, L.my, L.skip_on, sink, L.local_rows,
@@ -2066,8 +2068,15 @@ static cudaError_t launch_t(const RenderLaunch& L, cudaStream_t stream) {
         return cudaLaunchKernelEx(&cfg, kernel, *L.p, vol, grad, L.rp, L.occ, L.mx, L.my, L.skip_on, sink, cnt, fw,
                                   hits, tex, L.seq, nfh * 4u, (unsigned)((long long)L.local_rows * L.p->width));
     };
-    if (grad != nullptr) e = launch_b(shade_kernel<T, OP, INTERP, true>);
-    else e = launch_b(shade_kernel<T, OP, INTERP, false>);
+    if (grad != nullptr) {
+        if constexpr (INTERP == VC_TRILINEAR) {
+            e = cnt ? launch_b(shade_kernel<T, OP, INTERP, true, true>) : launch_b(shade_kernel<T, OP, INTERP, true, false>);
+        } else {
+            e = launch_b(shade_kernel<T, OP, INTERP, true>);
+        }
+    } else {
+        e = launch_b(shade_kernel<T, OP, INTERP, false>);
+    }
     if (e != cudaSuccess) return e;
     if (L.ev[2]) cudaEventRecord(L.ev[2], stream);
     return cudaGetLastError();
