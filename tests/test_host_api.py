@@ -198,3 +198,18 @@ def test_generate_ray_matches_reference_kats():
         vc.generate_ray(cam, 101, 0, 101, 101)
     cam = vc.Camera(eye=(0, 0, 10), target=(0, 0, 0), azimuth=90.0)
     assert vc.generate_ray(cam, 8, 8, 17, 17).origin == pytest.approx([10, 0, 0], abs=1e-9)
+
+
+def test_cross3_is_np_cross_bit_for_bit():
+    """camera_basis's hand-written 3-vector cross product equals np.cross
+    bit for bit (signed zeros included): the device consumes the basis."""
+    from paper_1609_01317_b200.raycast import _cross3
+
+    rng = np.random.default_rng(7)
+    vecs = [rng.normal(size=3) * s for s in (1e-300, 1e-8, 1.0, 1e8, 1e300) for _ in range(400)]
+    vecs += [np.array(v, np.float64) for v in ((0.0, -0.0, 1.0), (-0.0, 0.0, -0.0), (1.0, 0.0, 0.0),
+                                               (0.0, 1.0, 0.0), (-1.0, -0.0, 2.0))]
+    for a, b in zip(vecs, vecs[::-1]):
+        want = np.cross(a, b)
+        got = _cross3(a, b)
+        assert np.array_equal(want.view(np.int64), got.view(np.int64)), (a, b)
