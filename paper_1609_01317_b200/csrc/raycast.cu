@@ -855,7 +855,12 @@ __device__ __forceinline__ int skip_fx(int k, const int c[3], const float f[3], 
     int kn = k + 1;
     if (dt > 0.0f) {
         const float xs = __fmul_rn(dt, inv_coarse);
-        kn = xs < 0x1p30f ? max(kn, k + __float2int_ru(xs)) : 0x40000000;
+        // ceil(xs) on the FMA pipe (F2I is an XU op): 2^23 + x rounded up has
+        // ceil(x) as its integer part for 0 <= x <= 2^23; a jump clamped to
+        // 2^23 lattice steps still passes klast (< 2^19), so the ray ends
+        // exactly as with the full jump
+        const float xc = fminf(xs, 0x1p23f);
+        kn = max(kn, k + (__float_as_int(__fadd_ru(xc, 0x1p23f)) - 0x4b000000));
     }
     return kn;
 }
@@ -1382,13 +1387,19 @@ __global__ void __launch_bounds__(128, VC_FH_MINB) firsthit_kernel(const __grid_
     __shared__ FxLanes fxs;
     __shared__ double s_rhw[2];  // RN(1/width), RN(1/height)
     __shared__ int s_admit;      // fx_frame_admits
+    __shared__ float s_icf;      // (float)(1 / coarse): read at skip events (kept in a register, it was
+                                 // re-derived from the float64 value by an XU conversion at each)
     const int me = threadIdx.x;
     if (fxw && me == 0) {
         s_rhw[0] = __drcp_rn((double)P.width);
         s_rhw[1] = __drcp_rn((double)P.height);
         s_admit = fx_frame_admits(P, rp0) ? 1 : 0;
+        s_icf = C.sk.inv_coarse_f;
     }
-    if (fxw) __syncthreads();
+    if (fxw) {
+        __syncthreads();
+        C.sk.inv_coarse_f = s_icf;
+    }
     int kf = 0;         // lattice index of the fixed-point walk
     bool pend = false;  // paused for a float64 sample (fx_exact_step)
     int px = 0, lr = 0;
