@@ -96,6 +96,16 @@ __device__ __forceinline__ double ceil_pos(double x) {
 // conservativeness matters here, not bit-exactness.
 // LAZY (shade stage, few skip events per ray): the reciprocal speeds are
 // recomputed here from the direction instead of living in registers
+// RN(1/x) pinned to where it is written: the compiler hoists a plain
+// __drcp_rn of the (per-ray) direction out of the rare skip branch to every
+// resolve step of the shade loop (ncu: three MUFU.RCP64H + Newton chains per
+// shade).  Same instruction (rcp.rn.f64), same value.
+__device__ __forceinline__ double drcp_rn_here(double x) {
+    double r;
+    asm volatile("rcp.rn.f64 %0, %1;" : "=d"(r) : "d"(x));
+    return r;
+}
+
 template <bool LAZY = false>
 __device__ __forceinline__ double skip_to(double t, double k, double base, const Skip& sk, const RayPos& rp,
                                           const double p[3], const int c[3], int d) {
@@ -105,7 +115,7 @@ __device__ __forceinline__ double skip_to(double t, double k, double base, const
 #pragma unroll
     for (int a = 0; a < 3; a++) {
         const int lo = (c[a] >> MC_SHIFT) << MC_SHIFT;
-        const double ib = LAZY ? (rp.d[a] == 0.0 ? 0.0 : dmul(rp.s[a], __drcp_rn(rp.d[a]))) : sk.ib[a];
+        const double ib = LAZY ? (rp.d[a] == 0.0 ? 0.0 : dmul(rp.s[a], drcp_rn_here(rp.d[a]))) : sk.ib[a];
         // the box face ahead, in voxel units (branch-free: selects, one exact
         // int -> double on the FP64 pipe); a zero direction adds no limit
         const bool up = ib > 0.0;
